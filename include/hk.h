@@ -1,0 +1,177 @@
+/*
+ * hk.h -- exact multiprecision Hankel / Toeplitz / circulant matrix-vector product on B200.
+ *
+ * The operation (PAPER.md = G. Beliakov, arXiv:1402.5287; "P:NN" = PAPER.md line NN):
+ *   Hankel    y = A_H x,  A_H[i][j] = a_{i+j-1}            (schoolbook P:87-90, read
+ *                                                           as y_i = sum_j a_{i+j-1} x_j)
+ *   Toeplitz  y = A_T x,  A_T[i][j] = a_{n-i+j}
+ *   Circulant y = A_C x,  A_C[i][j] = c_{((i-j) mod n)+1}  (n x n, first column c)
+ * Every entry is a multiprecision fixed-point number a = B0 * sum_k B^k a_k with B = 2^64
+ * and B0 = 2^-P.  The result is exact (no rounding): y_i = Y_i * 2^-2P.
+ *
+ * LAYOUT (all arrays row-major, C-contiguous):
+ *   * a vector of `count` numbers is  mag: uint64_t[count][L]  (limb 0 least significant,
+ *     L = hk_limbs(P) = ceil(P/64))  plus  sign: int8_t[count]  in {-1, 0, +1};
+ *     value = sign * mag * 2^-P.  Inputs must satisfy sign == 0 <=> mag == 0, and every bit >= P
+ *     must be zero (violations are DATA errors, see below).
+ *   * outputs use Ly = hk_out_limbs(P) = 2L + 1 limbs: value = sign * mag * 2^-2P, canonical
+ *     (sign 0 iff the value is 0; |Y| < n (2^P-1)^2 always fits).
+ *
+ * OWNERSHIP: the caller owns every buffer.  Unless a function says HOST, all array pointers are
+ *   DEVICE pointers (e.g. torch CUDA tensors) on the current device.  The library allocates no
+ *   device memory and keeps no global mutable state; all per-problem state (plan header,
+ *   twiddle tables, transform-domain intermediates, status word) lives in the caller's
+ *   workspace `ws`.  y must not overlap a, c or x.  A workspace may be used by one stream at a
+ *   time; distinct workspaces may run concurrently.
+ *
+ * STREAMS: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *   matvec calls are asynchronous and stream-ordered; they never synchronise the host except
+ *   hk_workspace_status and hk_matvec_host (documented there).
+ *
+ * ERRORS: every function returns an hk_status (int32_t).  ARGUMENT errors are returned
+ *   synchronously before anything is enqueued: n < 1, P < 1, null pointers, overlapping y,
+ *   undersized workspace (HK_EINVAL / HK_ENOMEM).  Capacity failures (no exact plan, see
+ *   hk_plan) return HK_EUNSUPPORTED.  Launch failures return HK_ECUDA.  DATA errors
+ *   (non-canonical inputs: bits >= P set, sign outside {-1,0,1}, sign/magnitude mismatch) and a
+ *   workspace initialised for a different problem are detected on the device during the call
+ *   and recorded in the workspace status word, read by hk_workspace_status; y is unspecified
+ *   when that status is not HK_OK.  No C++ exception crosses this ABI.
+ *
+ * METHOD: each mantissa is cut into w-bit slices (w <= 65);
+ *   the product becomes an exact 2-D convolution over (matrix index x slice) computed as a
+ *   5-prime 31-bit number-theoretic transform (slice NTT of length N2 per entry, matrix-index
+ *   NTT of length N1 per transformed column, pointwise Montgomery product, inverse NTTs),
+ *   recombined by Garner CRT into signed coefficients and carried into exact limbs.  The planner
+ *   proves 2 n Ls (2^w - 1)^2 < p1 p2 p3 p4 p5 for every call.
+ */
+#ifndef HK_H
+#define HK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HK_OK = 0,
+    HK_EINVAL = -1,        /* bad argument / workspace not initialised for this problem     */
+    HK_ERANGE = -2,        /* data error: non-canonical input mantissa or sign                */
+    HK_ENOMEM = -3,        /* workspace too small                                             */
+    HK_EUNSUPPORTED = -4,  /* no exact plan for (kind, m, n, P) within the supported limits   */
+    HK_ECUDA = -5          /* a CUDA call or kernel launch failed                             */
+} hk_status;
+
+typedef enum { HK_HANKEL = 0, HK_TOEPLITZ = 1, HK_CIRCULANT = 2 } hk_kind;
+
+/* hk_workspace_size / hk_workspace_init flags */
+#define HK_WS_STAGING 1u   /* also reserve device staging buffers for hk_matvec_host */
+
+/* The plan the library chose for a problem (filled by hk_plan; all sizes in elements). */
+typedef struct {
+    int32_t kind;          /* hk_kind                                                          */
+    int32_t P;             /* mantissa bits                                                    */
+    int64_t m;             /* output rows (n for square kinds; window rows for rect Hankel)    */
+    int64_t n;             /* columns = length of x                                            */
+    int64_t a_count;       /* entries of the defining vector: m+n-1 (Hankel/Toeplitz), n (circ)*/
+    int32_t L;             /* input limbs  = ceil(P/64)                                        */
+    int32_t Ly;            /* output limbs = 2L+1                                              */
+    int32_t k_primes;      /* NTT primes (5)                                                   */
+    int32_t w;             /* slice width in bits (<= 65)                                      */
+    int32_t Ls;            /* slices per mantissa = ceil(P/w)                                  */
+    int32_t log_n2;        /* slice-dimension transform length N2 = 2^log_n2 >= 2Ls-1          */
+    int32_t log_n1;        /* matrix-index transform length N1 = 2^log_n1                      */
+    int32_t cyclic;        /* 1: circulant computed as a length-n cyclic convolution (n = N1)  */
+    int32_t fold;          /* 1: circulant via linear convolution folded at n                  */
+    double margin_bits;    /* log2(p1..p5) - log2(2 n Ls (2^w-1)^2) > 0                         */
+    uint64_t ws_bytes;     /* workspace bytes without staging                                  */
+    uint64_t ws_bytes_staging; /* workspace bytes with HK_WS_STAGING                           */
+} hk_plan_info;
+
+/* L = ceil(P/64) (l = ceil(b / log2 B)); returns -1 if P < 1. */
+int32_t hk_limbs(int32_t P);
+/* Ly = 2L + 1; returns -1 if P < 1. */
+int32_t hk_out_limbs(int32_t P);
+/* Static string for a status code. */
+const char *hk_status_string(int32_t status);
+
+/* Chooses (w, Ls, N2, N1) for kind / m x n / P and proves the exact-CRT capacity bound.
+ * m is the number of output rows: m == n for HK_TOEPLITZ / HK_CIRCULANT; for HK_HANKEL, m <= n is
+ * the row window of a rectangular m x n Hankel (a has m+n-1 entries; m == n is the square case).
+ * Pure host function.  HK_EUNSUPPORTED if no exact plan exists within the limits
+ * (N1 <= 32768, i.e. m+n-1 <= 32768 for Hankel/Toeplitz; P <= 66560). */
+int32_t hk_plan(int32_t kind, int64_t m, int64_t n, int32_t P, hk_plan_info *out);
+
+/* Bytes of device workspace for the problem (flags: HK_WS_STAGING). Pure host function. */
+int32_t hk_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags,
+                          size_t *bytes);
+
+/* Writes the plan header, the per-prime twiddle tables and a zero status word into ws
+ * (stream-ordered, asynchronous).  Must run once per (kind, m, n, P, flags) before the matvec
+ * calls that use ws.  ws: DEVICE pointer, 256-byte aligned, ws_bytes >= hk_workspace_size. */
+int32_t hk_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags,
+                          void *ws, size_t ws_bytes, void *stream);
+
+/* Synchronises `stream`, then reads the workspace's data-status word of the last call into
+ * *data_status (HK_OK, HK_ERANGE for bad input data, HK_EINVAL for a workspace initialised for a
+ * different problem).  Returns HK_ECUDA if the copy fails. */
+int32_t hk_workspace_status(void *ws, void *stream, int32_t *data_status);
+
+/* Square Hankel: a_mag[2n-1][L], a_sign[2n-1]; x_mag[n][L], x_sign[n]; y_mag[n][Ly], y_sign[n].
+ * y_i = sum_{j=1..n} a_{i+j-1} x_j.  DEVICE pointers. */
+int32_t hk_hankel_matvec(int64_t n, int32_t P,
+                         const uint64_t *a_mag, const int8_t *a_sign,
+                         const uint64_t *x_mag, const int8_t *x_sign,
+                         uint64_t *y_mag, int8_t *y_sign,
+                         void *ws, size_t ws_bytes, void *stream);
+
+/* Toeplitz: same shapes; y_i = sum_j a_{n-i+j} x_j.  Equals the Hankel product on the
+ * same vector with rows reversed.  DEVICE pointers. */
+int32_t hk_toeplitz_matvec(int64_t n, int32_t P,
+                           const uint64_t *a_mag, const int8_t *a_sign,
+                           const uint64_t *x_mag, const int8_t *x_sign,
+                           uint64_t *y_mag, int8_t *y_sign,
+                           void *ws, size_t ws_bytes, void *stream);
+
+/* Circulant: c_mag[n][L], c_sign[n] (first column); y_i = sum_j c_{((i-j) mod n)+1} x_j.
+ * DEVICE pointers. */
+int32_t hk_circulant_matvec(int64_t n, int32_t P,
+                            const uint64_t *c_mag, const int8_t *c_sign,
+                            const uint64_t *x_mag, const int8_t *x_sign,
+                            uint64_t *y_mag, int8_t *y_sign,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* Rectangular m x n Hankel window (the row-block shard of SURVEY.md 8(e)):
+ * a_mag[m+n-1][L]; y_i = sum_{j=1..n} a_{i+j-1} x_j for i = 1..m.  DEVICE pointers. */
+int32_t hk_hankel_rect_matvec(int64_t m, int64_t n, int32_t P,
+                              const uint64_t *a_mag, const int8_t *a_sign,
+                              const uint64_t *x_mag, const int8_t *x_sign,
+                              uint64_t *y_mag, int8_t *y_sign,
+                              void *ws, size_t ws_bytes, void *stream);
+
+/* End-to-end call with HOST buffers (same shapes as the kind's device call; for HK_HANKEL, m may
+ * be < n as in hk_hankel_rect_matvec).  Enqueues on `stream`: H2D copies of a and x into the
+ * workspace's staging area, the matvec, and D2H copies of y; then synchronises `stream` and
+ * returns the call's data status (so HK_ERANGE is returned directly).  Host buffers should be
+ * pinned (cudaHostAlloc / torch pin_memory) for asynchronous copies.  ws must have been sized and
+ * initialised with HK_WS_STAGING. */
+int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P,
+                       const uint64_t *a_mag_host, const int8_t *a_sign_host,
+                       const uint64_t *x_mag_host, const int8_t *x_sign_host,
+                       uint64_t *y_mag_host, int8_t *y_sign_host,
+                       void *ws, size_t ws_bytes, void *stream);
+
+/* Companion A6: direct schoolbook limb-product matvec on the GPU, no
+ * transform: y_i = sum_j A_{idx(i,j)} X_j with 32-bit limb products and wide column sums.
+ * kind / m / n / shapes as above (HK_HANKEL with m < n = rectangular window).  Needs no
+ * workspace; data errors are not checked (inputs must be canonical).  DEVICE pointers. */
+int32_t hk_schoolbook_matvec(int32_t kind, int64_t m, int64_t n, int32_t P,
+                             const uint64_t *a_mag, const int8_t *a_sign,
+                             const uint64_t *x_mag, const int8_t *x_sign,
+                             uint64_t *y_mag, int8_t *y_sign, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HK_H */

@@ -1,0 +1,277 @@
+"""paper_1402_5287_b200 -- exact multiprecision Hankel/Toeplitz/circulant matvec on B200.
+
+Thin ctypes binding over the C ABI of ``include/hk.h`` (``lib/libhk.so``, built in-tree by
+``_build.build()`` / ``__graft_entry__.build()``).  Every step of the product runs in the
+library's CUDA kernels; this module only marshals torch tensors (device memory, the current
+stream) into plain pointers.  There is NO CPU fallback: importing the package fails loudly when
+the library is missing, and every call checks its status code.
+
+Layout: a vector of ``count`` mantissas is ``mag`` uint64[count, L]
+(limb 0 least significant, L = ceil(P/64)) + ``sign`` int8[count]; value = sign*mag*2^-P.
+Outputs have Ly = 2L+1 limbs and value = sign*mag*2^-2P.  torch has limited uint64 support, so
+magnitudes may be passed as torch.int64 or torch.uint64 (same bits).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from ._build import LIB as _LIB_PATH
+
+HK_OK, HK_EINVAL, HK_ERANGE, HK_ENOMEM, HK_EUNSUPPORTED, HK_ECUDA = 0, -1, -2, -3, -4, -5
+HANKEL, TOEPLITZ, CIRCULANT = 0, 1, 2
+WS_STAGING = 1
+
+
+class HKError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {status_string(code)} ({code})")
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("P", ctypes.c_int32), ("m", ctypes.c_int64),
+                ("n", ctypes.c_int64), ("a_count", ctypes.c_int64), ("L", ctypes.c_int32),
+                ("Ly", ctypes.c_int32), ("k_primes", ctypes.c_int32), ("w", ctypes.c_int32),
+                ("Ls", ctypes.c_int32), ("log_n2", ctypes.c_int32), ("log_n1", ctypes.c_int32),
+                ("cyclic", ctypes.c_int32), ("fold", ctypes.c_int32),
+                ("margin_bits", ctypes.c_double), ("ws_bytes", ctypes.c_uint64),
+                ("ws_bytes_staging", ctypes.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"libhk.so not built ({_LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    sig = {
+        "hk_limbs": (i32, [i32]),
+        "hk_out_limbs": (i32, [i32]),
+        "hk_status_string": (ctypes.c_char_p, [i32]),
+        "hk_plan": (i32, [i32, i64, i64, i32, ctypes.POINTER(PlanInfo)]),
+        "hk_workspace_size": (i32, [i32, i64, i64, i32, ctypes.c_uint32, ctypes.POINTER(sz)]),
+        "hk_workspace_init": (i32, [i32, i64, i64, i32, ctypes.c_uint32, vp, sz, vp]),
+        "hk_workspace_status": (i32, [vp, vp, ctypes.POINTER(i32)]),
+        "hk_hankel_matvec": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_toeplitz_matvec": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_circulant_matvec": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_rect_matvec": (i32, [i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_matvec_host": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_schoolbook_matvec": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+_lib = _load()
+EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_workspace_size",
+            "hk_workspace_init", "hk_workspace_status", "hk_hankel_matvec", "hk_toeplitz_matvec",
+            "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host",
+            "hk_schoolbook_matvec")
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def status_string(code: int) -> str:
+    return _lib.hk_status_string(int(code)).decode()
+
+
+def _check(code: int, where: str) -> None:
+    if code != HK_OK:
+        raise HKError(code, where)
+
+
+def limbs(P: int) -> int:
+    return int(_lib.hk_limbs(P))
+
+
+def out_limbs(P: int) -> int:
+    return int(_lib.hk_out_limbs(P))
+
+
+def plan(kind: int, n: int, P: int, m: int | None = None) -> dict:
+    """The exact plan (w, Ls, N1, N2, margin) the library uses; pure host call."""
+    info = PlanInfo()
+    _check(_lib.hk_plan(kind, n if m is None else m, n, P, ctypes.byref(info)), "hk_plan")
+    return info.as_dict()
+
+
+def workspace_size(kind: int, n: int, P: int, m: int | None = None, flags: int = 0) -> int:
+    out = ctypes.c_size_t()
+    _check(_lib.hk_workspace_size(kind, n if m is None else m, n, P, flags, ctypes.byref(out)),
+           "hk_workspace_size")
+    return int(out.value)
+
+
+def _stream_ptr(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return int(s.cuda_stream)
+
+
+class Workspace:
+    """Caller-owned device workspace (a torch uint8 CUDA tensor) initialised for one problem."""
+
+    def __init__(self, kind: int, n: int, P: int, m: int | None = None, flags: int = 0,
+                 device=None, stream=None):
+        import torch
+        self.kind, self.n, self.P = int(kind), int(n), int(P)
+        self.m = self.n if m is None else int(m)
+        self.flags = int(flags)
+        self.nbytes = workspace_size(kind, n, P, m=self.m, flags=flags)
+        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8,
+                               device=device or torch.device("cuda", torch.cuda.current_device()))
+        base = self.buf.data_ptr()
+        self.ptr = (base + 255) & ~255
+        _check(_lib.hk_workspace_init(kind, self.m, self.n, P, flags, self.ptr, self.nbytes,
+                                      _stream_ptr(stream)), "hk_workspace_init")
+
+    def status(self, stream=None) -> int:
+        v = ctypes.c_int32()
+        _check(_lib.hk_workspace_status(self.ptr, _stream_ptr(stream), ctypes.byref(v)),
+               "hk_workspace_status")
+        return int(v.value)
+
+
+def _dev_ptr(t, dtypes, shape, name):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name}: expected a CUDA tensor")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name}: dtype {t.dtype} not in {dtypes}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)} != {tuple(shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    return t.data_ptr()
+
+
+def _mag_dtypes():
+    import torch
+    return (torch.int64, torch.uint64)
+
+
+def _run(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None,
+         check=True):
+    import torch
+    n = int(x_mag.shape[0])
+    m = n if m is None else int(m)
+    L = limbs(P)
+    Ly = out_limbs(P)
+    na = (n if kind == CIRCULANT else m + n - 1)
+    args = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (n,), "x_sign")]
+    if out is None:
+        out = (torch.empty((m, Ly), dtype=a_mag.dtype, device=a_mag.device),
+               torch.empty((m,), dtype=torch.int8, device=a_mag.device))
+    args += [_dev_ptr(out[0], _mag_dtypes(), (m, Ly), "y_mag"),
+             _dev_ptr(out[1], (torch.int8,), (m,), "y_sign")]
+    if ws is None:
+        ws = Workspace(kind, n, P, m=m, stream=stream)
+    if (ws.kind, ws.m, ws.n, ws.P) != (kind, m, n, P):
+        raise ValueError("workspace was initialised for a different problem")
+    sp = _stream_ptr(stream)
+    if kind == HANKEL and m != n:
+        rc = _lib.hk_hankel_rect_matvec(m, n, P, *args, ws.ptr, ws.nbytes, sp)
+    else:
+        fn = {HANKEL: _lib.hk_hankel_matvec, TOEPLITZ: _lib.hk_toeplitz_matvec,
+              CIRCULANT: _lib.hk_circulant_matvec}[kind]
+        rc = fn(n, P, *args, ws.ptr, ws.nbytes, sp)
+    _check(rc, "matvec")
+    if check:
+        _check(ws.status(stream), "matvec data status")
+    return out
+
+
+def hankel_matvec(a_mag, a_sign, x_mag, x_sign, P, out=None, ws=None, stream=None, check=True):
+    """y = A_H x, A_H[i][j] = a_{i+j-1}; a has 2n-1 entries."""
+    return _run(HANKEL, a_mag, a_sign, x_mag, x_sign, P, out=out, ws=ws, stream=stream, check=check)
+
+
+def toeplitz_matvec(a_mag, a_sign, x_mag, x_sign, P, out=None, ws=None, stream=None, check=True):
+    """y = A_T x, A_T[i][j] = a_{n-i+j}."""
+    return _run(TOEPLITZ, a_mag, a_sign, x_mag, x_sign, P, out=out, ws=ws, stream=stream, check=check)
+
+
+def circulant_matvec(c_mag, c_sign, x_mag, x_sign, P, out=None, ws=None, stream=None, check=True):
+    """y = A_C x, A_C[i][j] = c_{((i-j) mod n)+1}."""
+    return _run(CIRCULANT, c_mag, c_sign, x_mag, x_sign, P, out=out, ws=ws, stream=stream, check=check)
+
+
+def hankel_rect_matvec(a_mag, a_sign, x_mag, x_sign, P, m, out=None, ws=None, stream=None,
+                       check=True):
+    """Rows 1..m of a Hankel product over the window a[0 .. m+n-2] (row-block shard)."""
+    return _run(HANKEL, a_mag, a_sign, x_mag, x_sign, P, m=m, out=out, ws=ws, stream=stream,
+                check=check)
+
+
+def matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None, check=True):
+    return _run(kind, a_mag, a_sign, x_mag, x_sign, P, m=m, out=out, ws=ws, stream=stream, check=check)
+
+
+def matvec_host(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None):
+    """End-to-end call with HOST (numpy or pinned torch CPU) buffers through hk_matvec_host:
+    H2D copies, the matvec and D2H copies happen inside the library call."""
+    n = int(x_mag.shape[0])
+    m = n if m is None else int(m)
+    Ly = out_limbs(P)
+
+    def hptr(a):
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+    if out is None:
+        out = (np.empty((m, Ly), dtype=np.uint64), np.empty((m,), dtype=np.int8))
+    if ws is None:
+        ws = Workspace(kind, n, P, m=m, flags=WS_STAGING, stream=stream)
+    if not ws.flags & WS_STAGING:
+        raise ValueError("workspace needs WS_STAGING for host-buffer calls")
+    rc = _lib.hk_matvec_host(kind, m, n, P, hptr(a_mag), hptr(a_sign), hptr(x_mag), hptr(x_sign),
+                             hptr(out[0]), hptr(out[1]), ws.ptr, ws.nbytes, _stream_ptr(stream))
+    _check(rc, "hk_matvec_host")
+    return out
+
+
+def schoolbook_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, stream=None):
+    """Companion A6: direct schoolbook limb products on the GPU (no transform)."""
+    import torch
+    n = int(x_mag.shape[0])
+    m = n if m is None else int(m)
+    L, Ly = limbs(P), out_limbs(P)
+    na = (n if kind == CIRCULANT else m + n - 1)
+    args = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (n,), "x_sign")]
+    if out is None:
+        out = (torch.empty((m, Ly), dtype=a_mag.dtype, device=a_mag.device),
+               torch.empty((m,), dtype=torch.int8, device=a_mag.device))
+    args += [_dev_ptr(out[0], _mag_dtypes(), (m, Ly), "y_mag"),
+             _dev_ptr(out[1], (torch.int8,), (m,), "y_sign")]
+    _check(_lib.hk_schoolbook_matvec(kind, m, n, P, *args, _stream_ptr(stream)),
+           "hk_schoolbook_matvec")
+    return out
+
+
+def to_device(mag: np.ndarray, sign: np.ndarray, device="cuda"):
+    """numpy (uint64 limbs, int8 signs) -> torch CUDA tensors (int64 view of the limbs)."""
+    import torch
+    m = torch.from_numpy(np.ascontiguousarray(mag).view(np.int64)).to(device)
+    s = torch.from_numpy(np.ascontiguousarray(sign, dtype=np.int8)).to(device)
+    return m, s
+
+
+def to_host(mag, sign) -> tuple[np.ndarray, np.ndarray]:
+    return (mag.cpu().numpy().view(np.uint64), sign.cpu().numpy())

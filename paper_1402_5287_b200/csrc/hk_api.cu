@@ -1,0 +1,411 @@
+// hk_api.cu -- the C ABI of include/hk.h: planner (exact-capacity proof), workspace layout,
+// argument validation and launch sequencing.  Host code only; kernels live in hk_ntt.cu and
+// hk_schoolbook.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "hk_internal.h"
+
+namespace hk {
+namespace {
+
+constexpr uint32_t kPrimesHost[kNumPrimes] = {2147352577u, 2146959361u, 2146041857u,
+                                              2144468993u, 2142502913u};
+
+uint32_t mulmod(uint32_t a, uint32_t b, uint32_t p) { return (uint32_t)(((uint64_t)a * b) % p); }
+uint32_t powmod(uint32_t b, uint64_t e, uint32_t p) {
+    uint32_t r = 1 % p;
+    b %= p;
+    while (e) {
+        if (e & 1) r = mulmod(r, b, p);
+        b = mulmod(b, b, p);
+        e >>= 1;
+    }
+    return r;
+}
+uint32_t invmod(uint32_t a, uint32_t p) { return powmod(a, p - 2, p); }  // p prime
+uint32_t shoup_q(uint32_t w, uint32_t p) { return (uint32_t)(((uint64_t)w << 32) / p); }
+
+uint32_t primitive_root(uint32_t p) {
+    std::vector<uint32_t> fac;
+    uint32_t r = p - 1;
+    for (uint32_t d = 2; (uint64_t)d * d <= r; ++d)
+        if (r % d == 0) {
+            fac.push_back(d);
+            while (r % d == 0) r /= d;
+        }
+    if (r > 1) fac.push_back(r);
+    for (uint32_t g = 2;; ++g) {
+        bool ok = true;
+        for (uint32_t q : fac)
+            if (powmod(g, (p - 1) / q, p) == 1) { ok = false; break; }
+        if (ok) return g;
+    }
+}
+
+// ---- tiny exact big-integer helpers for the capacity proof (little-endian u32 limbs)
+using Big = std::vector<uint32_t>;
+Big big_from(uint64_t v) { return Big{(uint32_t)v, (uint32_t)(v >> 32)}; }
+Big big_mul(const Big &a, const Big &b) {
+    Big r(a.size() + b.size(), 0);
+    for (size_t i = 0; i < a.size(); ++i) {
+        uint64_t c = 0;
+        for (size_t j = 0; j < b.size(); ++j) {
+            uint64_t t = (uint64_t)a[i] * b[j] + r[i + j] + c;
+            r[i + j] = (uint32_t)t;
+            c = t >> 32;
+        }
+        r[i + b.size()] += (uint32_t)c;
+    }
+    return r;
+}
+int big_cmp(Big a, Big b) {
+    while (a.size() < b.size()) a.push_back(0);
+    while (b.size() < a.size()) b.push_back(0);
+    for (size_t i = a.size(); i-- > 0;)
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    return 0;
+}
+Big big_pow2_minus1(int w) {  // 2^w - 1
+    Big r((w + 31) / 32 + 1, 0);
+    for (int b = 0; b < w; ++b) r[b / 32] |= 1u << (b % 32);
+    return r;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Plan *pl) {
+    if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || m < 1 || P < 1) return HK_EINVAL;
+    if (kind != HK_HANKEL && m != n) return HK_EINVAL;
+    std::memset(pl, 0, sizeof(*pl));
+    hk_plan_info &in = pl->info;
+    in.kind = kind;
+    in.P = P;
+    in.m = m;
+    in.n = n;
+    in.L = (P + 63) / 64;
+    in.Ly = 2 * in.L + 1;
+    in.k_primes = kNumPrimes;
+    in.a_count = kind == HK_CIRCULANT ? n : m + n - 1;
+    if (in.Ly > kK3Threads * kK3MaxChunk) return HK_EUNSUPPORTED;
+    // matrix-index transform length
+    int64_t need;
+    if (kind == HK_CIRCULANT) {
+        const bool pow2 = (n & (n - 1)) == 0;
+        if (pow2 && n >= (1 << kMinLogN1)) {
+            in.cyclic = 1;
+            need = n;
+        } else {
+            in.fold = 1;
+            need = 2 * n - 1;
+        }
+        pl->x_reversed = 0;
+        pl->out_off = 0;
+    } else {
+        need = in.a_count;
+        pl->x_reversed = 1;
+        pl->out_off = n - 1;
+    }
+    pl->reverse_out = kind == HK_TOEPLITZ;
+    int lg1 = kMinLogN1;
+    while ((int64_t(1) << lg1) < need) ++lg1;
+    if (lg1 > kMaxLogN1) return HK_EUNSUPPORTED;
+    in.log_n1 = lg1;
+    // slice width / slice transform: smallest N2 with an exact plan
+    Big M = big_from(1);
+    for (int k = 0; k < kNumPrimes; ++k) M = big_mul(M, big_from(kPrimesHost[k]));
+    double logM = 0;
+    for (int k = 0; k < kNumPrimes; ++k) logM += std::log2((double)kPrimesHost[k]);
+    bool found = false;
+    for (int lg2 = kMinLogN2; lg2 <= kMaxLogN2 && !found; ++lg2) {
+        const int64_t lsmax = (int64_t(1) << lg2) / 2;  // 2 Ls - 1 <= N2
+        int64_t w = (P + lsmax - 1) / lsmax;
+        if (w < 1) w = 1;
+        for (; w <= kMaxW; ++w) {  // smallest w that fits this N2 first (largest margin)
+            const int64_t Ls = (P + w - 1) / w;
+            if (2 * Ls - 1 > (int64_t(1) << lg2)) continue;
+            Big wm = big_pow2_minus1((int)w);
+            Big B = big_mul(big_mul(wm, wm), big_mul(big_from((uint64_t)(2 * n)), big_from((uint64_t)Ls)));
+            if (big_cmp(B, M) < 0) {
+                in.w = (int32_t)w;
+                in.Ls = (int32_t)Ls;
+                in.log_n2 = lg2;
+                in.margin_bits = logM - (1.0 + std::log2((double)n) + std::log2((double)Ls) +
+                                         2.0 * std::log2(std::ldexp(1.0, (int)w) - 1.0));
+                found = true;
+            }
+            break;  // larger w for the same N2 only shrinks the margin
+        }
+    }
+    if (!found) return HK_EUNSUPPORTED;
+    const int64_t N2 = int64_t(1) << in.log_n2;
+    const int64_t S2 = 2 * (int64_t)in.Ls - 1;
+    pl->ldA = (in.a_count + 31) / 32 * 32;
+    pl->ldX = (n + 31) / 32 * 32;
+    pl->ldY = (m + 31) / 32 * 32;
+    pl->ldS = (S2 + 3) / 4 * 4;
+    const int64_t N1 = int64_t(1) << in.log_n1;
+    size_t off = align256(sizeof(WsHeader));
+    pl->off_tw = off;
+    off = align256(off + (size_t)kNumPrimes * 2 * (N1 + N2) * sizeof(uint2));
+    pl->off_A = off;
+    size_t szA = (size_t)kNumPrimes * N2 * pl->ldA * 4;
+    const size_t szRes = (size_t)m * kNumPrimes * pl->ldS * 4;  // Yres aliases A^
+    if (szRes > szA) szA = szRes;
+    off = align256(off + szA);
+    pl->off_X = off;
+    off = align256(off + (size_t)kNumPrimes * N2 * pl->ldX * 4);
+    pl->off_Y = off;
+    off = align256(off + (size_t)kNumPrimes * N2 * pl->ldY * 4);
+    pl->off_end = off;
+    pl->off_stage = off;
+    const size_t L = in.L, Ly = in.Ly;
+    pl->st_amag = off;  off = align256(off + (size_t)in.a_count * L * 8);
+    pl->st_asign = off; off = align256(off + (size_t)in.a_count);
+    pl->st_xmag = off;  off = align256(off + (size_t)n * L * 8);
+    pl->st_xsign = off; off = align256(off + (size_t)n);
+    pl->st_ymag = off;  off = align256(off + (size_t)m * Ly * 8);
+    pl->st_ysign = off; off = align256(off + (size_t)m);
+    pl->off_end_staging = off;
+    in.ws_bytes = pl->off_end;
+    in.ws_bytes_staging = pl->off_end_staging;
+    (void)flags;
+    return HK_OK;
+}
+
+uint64_t plan_hash(int32_t kind, int64_t m, int64_t n, int32_t P) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) {
+        for (int i = 0; i < 8; ++i) { h ^= (v >> (8 * i)) & 0xff; h *= 1099511628211ull; }
+    };
+    mix((uint64_t)kind); mix((uint64_t)m); mix((uint64_t)n); mix((uint64_t)P);
+    return h;
+}
+
+void fill_params(const Plan &pl, void *ws, Params *prm) {
+    std::memset(prm, 0, sizeof(*prm));
+    const hk_plan_info &in = pl.info;
+    prm->kind = in.kind; prm->P = in.P; prm->L = in.L; prm->Ly = in.Ly;
+    prm->m = in.m; prm->n = in.n; prm->a_count = in.a_count;
+    prm->w = in.w; prm->Ls = in.Ls; prm->S2 = 2 * in.Ls - 1;
+    prm->log_n1 = in.log_n1; prm->log_n2 = in.log_n2;
+    prm->N1 = 1 << in.log_n1; prm->N2 = 1 << in.log_n2;
+    prm->cyclic = in.cyclic; prm->fold = in.fold;
+    prm->reverse_out = pl.reverse_out; prm->x_reversed = pl.x_reversed;
+    prm->out_off = pl.out_off;
+    prm->ldA = pl.ldA; prm->ldX = pl.ldX; prm->ldY = pl.ldY; prm->ldS = pl.ldS;
+    prm->hash = plan_hash(in.kind, in.m, in.n, in.P);
+    char *base = (char *)ws;
+    prm->hdr = (WsHeader *)base;
+    prm->tw = (const uint2 *)(base + pl.off_tw);
+    prm->Ahat = (uint32_t *)(base + pl.off_A);
+    prm->Yres = (uint32_t *)(base + pl.off_A);
+    prm->Xhat = (uint32_t *)(base + pl.off_X);
+    prm->Yhat = (uint32_t *)(base + pl.off_Y);
+    const uint64_t N12 = (uint64_t)prm->N1 * (uint64_t)prm->N2;
+    for (int k = 0; k < kNumPrimes; ++k) {
+        const uint32_t p = kPrimesHost[k];
+        PrimeConsts &c = prm->pc[k];
+        c.p = p;
+        uint32_t inv = 1;  // Newton: p^-1 mod 2^32
+        for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+        c.pneg = 0u - inv;
+        const uint32_t r32 = (uint32_t)((uint64_t(1) << 32) % p);
+        const uint32_t r64 = mulmod(r32, r32, p);
+        const uint32_t f = mulmod(r32, invmod((uint32_t)(N12 % p), p), p);  // 2^32 (N1 N2)^-1
+        const uint32_t wa[3] = {1u, r32, r64};
+        for (int d = 0; d < 3; ++d) {
+            c.fa[d] = wa[d];
+            c.fa_q[d] = shoup_q(wa[d], p);
+            c.fx[d] = mulmod(wa[d], f, p);
+            c.fx_q[d] = shoup_q(c.fx[d], p);
+        }
+    }
+    for (int j = 0; j < kNumPrimes; ++j)
+        for (int k = 0; k < kNumPrimes; ++k) {
+            if (j >= k) continue;
+            const uint32_t v = invmod(kPrimesHost[j] % kPrimesHost[k], kPrimesHost[k]);
+            prm->gc.inv[j][k] = v;
+            prm->gc.inv_q[j][k] = shoup_q(v, kPrimesHost[k]);
+        }
+}
+
+bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
+    const char *pa = (const char *)a, *pb = (const char *)b;
+    return pa < pb + nb && pb < pa + na;
+}
+
+int run_matvec(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
+               const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
+               uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, 0, &pl);
+    if (rc) return rc;
+    if (((uintptr_t)ws & 255) != 0) return HK_EINVAL;
+    if (ws_bytes < pl.info.ws_bytes) return HK_ENOMEM;
+    const size_t L = pl.info.L, Ly = pl.info.Ly;
+    const size_t ya = (size_t)m * Ly * 8, ys = (size_t)m;
+    const size_t aa = (size_t)pl.info.a_count * L * 8, as = (size_t)pl.info.a_count;
+    const size_t xa = (size_t)n * L * 8, xs = (size_t)n;
+    if (overlaps(y_mag, ya, a_mag, aa) || overlaps(y_mag, ya, x_mag, xa) ||
+        overlaps(y_sign, ys, a_sign, as) || overlaps(y_sign, ys, x_sign, xs) ||
+        overlaps(y_mag, ya, y_sign, ys) || overlaps(y_mag, ya, ws, pl.info.ws_bytes) ||
+        overlaps(y_sign, ys, ws, pl.info.ws_bytes))
+        return HK_EINVAL;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
+    prm.y_mag = y_mag; prm.y_sign = y_sign;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    return launch_ntt_path(prm, stream);
+}
+
+}  // namespace
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" {
+
+int32_t hk_limbs(int32_t P) { return P < 1 ? -1 : (P + 63) / 64; }
+int32_t hk_out_limbs(int32_t P) { return P < 1 ? -1 : 2 * ((P + 63) / 64) + 1; }
+
+const char *hk_status_string(int32_t s) {
+    switch (s) {
+        case HK_OK: return "HK_OK";
+        case HK_EINVAL: return "HK_EINVAL: invalid argument or workspace";
+        case HK_ERANGE: return "HK_ERANGE: non-canonical input data";
+        case HK_ENOMEM: return "HK_ENOMEM: workspace too small";
+        case HK_EUNSUPPORTED: return "HK_EUNSUPPORTED: no exact plan within limits";
+        case HK_ECUDA: return "HK_ECUDA: CUDA error";
+        default: return "unknown hk_status";
+    }
+}
+
+int32_t hk_plan(int32_t kind, int64_t m, int64_t n, int32_t P, hk_plan_info *out) {
+    if (!out) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, 0, &pl);
+    if (rc) return rc;
+    *out = pl.info;
+    return HK_OK;
+}
+
+int32_t hk_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags,
+                          size_t *bytes) {
+    if (!bytes) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, flags, &pl);
+    if (rc) return rc;
+    *bytes = (flags & HK_WS_STAGING) ? pl.info.ws_bytes_staging : pl.info.ws_bytes;
+    return HK_OK;
+}
+
+int32_t hk_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags,
+                          void *ws, size_t ws_bytes, void *stream) {
+    if (!ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, flags, &pl);
+    if (rc) return rc;
+    const size_t need = (flags & HK_WS_STAGING) ? pl.info.ws_bytes_staging : pl.info.ws_bytes;
+    if (ws_bytes < need) return HK_ENOMEM;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    uint32_t gens[kNumPrimes];
+    for (int k = 0; k < kNumPrimes; ++k) gens[k] = primitive_root(kPrimesHost[k]);
+    return launch_init(prm, gens, stream);
+}
+
+int32_t hk_workspace_status(void *ws, void *stream, int32_t *data_status) {
+    if (!ws || !data_status) return HK_EINVAL;
+    int32_t v = HK_ECUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(&v, &((WsHeader *)ws)->status, sizeof(v), cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return HK_ECUDA;
+    *data_status = v;
+    return HK_OK;
+}
+
+int32_t hk_hankel_matvec(int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
+                         const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
+                         int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    return run_matvec(HK_HANKEL, n, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
+                      ws_bytes, stream);
+}
+
+int32_t hk_toeplitz_matvec(int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
+                           const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
+                           int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    return run_matvec(HK_TOEPLITZ, n, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
+                      ws_bytes, stream);
+}
+
+int32_t hk_circulant_matvec(int64_t n, int32_t P, const uint64_t *c_mag, const int8_t *c_sign,
+                            const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
+                            int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    return run_matvec(HK_CIRCULANT, n, n, P, c_mag, c_sign, x_mag, x_sign, y_mag, y_sign, ws,
+                      ws_bytes, stream);
+}
+
+int32_t hk_hankel_rect_matvec(int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
+                              const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
+                              uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes,
+                              void *stream) {
+    return run_matvec(HK_HANKEL, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
+                      ws_bytes, stream);
+}
+
+int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag_host,
+                       const int8_t *a_sign_host, const uint64_t *x_mag_host,
+                       const int8_t *x_sign_host, uint64_t *y_mag_host, int8_t *y_sign_host,
+                       void *ws, size_t ws_bytes, void *stream) {
+    if (!a_mag_host || !a_sign_host || !x_mag_host || !x_sign_host || !y_mag_host ||
+        !y_sign_host || !ws)
+        return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_STAGING, &pl);
+    if (rc) return rc;
+    if (ws_bytes < pl.info.ws_bytes_staging) return HK_ENOMEM;
+    cudaStream_t st = (cudaStream_t)stream;
+    char *base = (char *)ws;
+    const size_t L = pl.info.L, Ly = pl.info.Ly, na = pl.info.a_count;
+    uint64_t *d_am = (uint64_t *)(base + pl.st_amag);
+    int8_t *d_as = (int8_t *)(base + pl.st_asign);
+    uint64_t *d_xm = (uint64_t *)(base + pl.st_xmag);
+    int8_t *d_xs = (int8_t *)(base + pl.st_xsign);
+    uint64_t *d_ym = (uint64_t *)(base + pl.st_ymag);
+    int8_t *d_ys = (int8_t *)(base + pl.st_ysign);
+    if (cudaMemcpyAsync(d_am, a_mag_host, na * L * 8, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(d_as, a_sign_host, na, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(d_xm, x_mag_host, (size_t)n * L * 8, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(d_xs, x_sign_host, (size_t)n, cudaMemcpyHostToDevice, st))
+        return HK_ECUDA;
+    rc = run_matvec(kind, m, n, P, d_am, d_as, d_xm, d_xs, d_ym, d_ys, ws, pl.info.ws_bytes, stream);
+    if (rc) return rc;
+    if (cudaMemcpyAsync(y_mag_host, d_ym, (size_t)m * Ly * 8, cudaMemcpyDeviceToHost, st) ||
+        cudaMemcpyAsync(y_sign_host, d_ys, (size_t)m, cudaMemcpyDeviceToHost, st))
+        return HK_ECUDA;
+    int32_t ds = HK_ECUDA;
+    rc = hk_workspace_status(ws, stream, &ds);
+    if (rc) return rc;
+    return ds;
+}
+
+int32_t hk_schoolbook_matvec(int32_t kind, int64_t m, int64_t n, int32_t P,
+                             const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
+                             const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign) return HK_EINVAL;
+    if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || m < 1 || P < 1) return HK_EINVAL;
+    if (kind != HK_HANKEL && m != n) return HK_EINVAL;
+    return launch_schoolbook(kind, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// hk_internal.h -- plan / parameter structures shared by the host API (hk_api.cu) and the
+// kernels (hk_ntt.cu, hk_schoolbook.cu).  Not part of the public ABI (include/hk.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/hk.h"
+
+namespace hk {
+
+constexpr int kNumPrimes = 5;
+constexpr uint64_t kWsMagic = 0x484b5753504c414eull;  // "HKWSPLAN"
+constexpr int kMaxLogN1 = 15;                           // N1 <= 32768 (K2 register budget)
+constexpr int kMinLogN1 = 6;
+constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
+constexpr int kMinLogN2 = 5;
+constexpr int kMaxW = 65;                               // a slice spans at most two limbs
+constexpr int kK3Threads = 512;                         // CRT/carry block
+constexpr int kK3MaxChunk = 8;                          // limbs per thread -> Ly <= 4096
+
+struct PrimeConsts {
+    uint32_t p, pneg;          // modulus, -p^-1 mod 2^32 (Montgomery)
+    uint32_t fa[3], fa_q[3];   // a digit weights 1, 2^32, 2^64 mod p (+ Shoup quotients)
+    uint32_t fx[3], fx_q[3];   // x digit weights times 2^32 (N1 N2)^-1 mod p (+ quotients)
+};
+
+struct GarnerConsts {
+    uint32_t inv[kNumPrimes][kNumPrimes];    // p_j^-1 mod p_k, j < k
+    uint32_t inv_q[kNumPrimes][kNumPrimes];  // Shoup quotients
+};
+
+struct WsHeader {  // first 256 bytes of a workspace
+    uint64_t magic;
+    uint64_t hash;
+    int32_t status;
+    int32_t pad_[59];
+};
+
+// Everything a launch needs, passed by value.
+struct Params {
+    // problem
+    int32_t kind, P, L, Ly;
+    int64_t m, n, a_count;
+    // plan
+    int32_t w, Ls, S2;           // S2 = 2Ls-1 output slices
+    int32_t log_n1, log_n2, N1, N2;
+    int32_t cyclic, fold, reverse_out, x_reversed;
+    int64_t out_off;             // first needed index of the matrix-index convolution
+    int64_t ldA, ldX, ldY, ldS;  // leading dims (elements) of the transform-domain arrays
+    uint64_t hash;
+    // inputs / outputs (device)
+    const uint64_t *a_mag;
+    const int8_t *a_sign;
+    const uint64_t *x_mag;
+    const int8_t *x_sign;
+    uint64_t *y_mag;
+    int8_t *y_sign;
+    // workspace regions
+    WsHeader *hdr;
+    const uint2 *tw;             // per prime: [N2 fwd | N2 inv | N1 fwd | N1 inv]
+    uint32_t *Ahat, *Xhat, *Yhat, *Yres;
+    PrimeConsts pc[kNumPrimes];
+    GarnerConsts gc;
+};
+
+struct Plan {
+    hk_plan_info info;
+    int64_t out_off;
+    int32_t reverse_out, x_reversed;
+    int64_t ldA, ldX, ldY, ldS;
+    size_t off_tw, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
+    size_t st_amag, st_asign, st_xmag, st_xsign, st_ymag, st_ysign;
+};
+
+// kernels (hk_ntt.cu)
+int launch_init(const Params &prm, const uint32_t *gens, void *stream);
+int launch_ntt_path(const Params &prm, void *stream);
+// companion (hk_schoolbook.cu)
+int launch_schoolbook(int kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
+                      const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
+                      uint64_t *y_mag, int8_t *y_sign, void *stream);
+
+}  // namespace hk

@@ -1,0 +1,191 @@
+// hk_modarith.cuh -- 31-bit prime-field arithmetic and shared-memory NTT passes for sm_100a.
+//
+// The exact 2-D convolution runs over k = 5 primes p < 2^31 with
+// 2^17 | p - 1, so every power-of-two transform length up to 2^17 has a root of unity.
+// Residues are kept fully reduced in [0, p): with p < 2^31 the sum of two residues fits in
+// 32 bits, the difference plus p as well, so no 64-bit arithmetic appears in a butterfly.
+//
+//   Shoup product  x*W mod p with W' = floor(W 2^32 / p):  q = hi(x W'), r = x W - q p in [0, 2p)
+//                  (3 IMAD; valid for every 32-bit x)
+//   Montgomery     a*b*2^-32 mod p (a, b < p):            3 IMAD (IMAD.WIDE + IMAD + IMAD.WIDE)
+//   GS butterfly   (u, v) -> (u + v, (u - v) W)            forward DIF, natural -> bit-reversed
+//   CT butterfly   (u, v) -> (u + v W, u - v W)            inverse DIT, bit-reversed -> natural
+#pragma once
+#include <cstdint>
+
+#define HK_DEV __device__ __forceinline__
+
+namespace hk {
+
+constexpr int kPrimes = 5;
+// p = c * 2^17 + 1 < 2^31, the five largest such primes; log2(prod) = 154.993
+constexpr uint32_t kP[kPrimes] = {2147352577u, 2146959361u, 2146041857u, 2144468993u,
+                                  2142502913u};
+
+// Padded shared-memory index: one spare word after every 32 keeps the strided radix passes
+// (stride S = 1..16 between a thread's points) free of bank conflicts.
+HK_DEV int pad(int i) { return i + (i >> 5); }
+__host__ __device__ constexpr int padded_len(int n) { return n + (n >> 5); }
+
+HK_DEV uint32_t red1(uint32_t x, uint32_t p) { return min(x, x - p); }  // [0,2p) -> [0,p)
+HK_DEV uint32_t addm(uint32_t a, uint32_t b, uint32_t p) {                // [0,p)^2 -> [0,p)
+    uint32_t s = a + b;
+    return min(s, s - p);
+}
+HK_DEV uint32_t subm(uint32_t a, uint32_t b, uint32_t p) {                // [0,p)^2 -> [0,p)
+    uint32_t d = a - b;
+    return min(d, d + p);
+}
+HK_DEV uint32_t shoup(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {  // -> [0, 2p)
+    uint32_t q = __umulhi(x, wq);
+    return x * w - q * p;
+}
+HK_DEV uint32_t mont(uint32_t a, uint32_t b, uint32_t p, uint32_t pneg) { // a b 2^-32, [0,p)
+    uint64_t z = (uint64_t)a * b;
+    uint32_t m = (uint32_t)z * pneg;
+    uint64_t t = z + (uint64_t)m * p;  // < 2^64 since a, b < p < 2^31
+    return red1((uint32_t)(t >> 32), p);
+}
+
+// Gentleman-Sande (DIF) butterfly, inputs/outputs in [0, p).
+HK_DEV void gs_bfly(uint32_t &u, uint32_t &v, uint2 w, uint32_t p) {
+    uint32_t d = u - v + p;  // [1, 2p)
+    u = addm(u, v, p);
+    v = red1(shoup(d, w.x, w.y, p), p);
+}
+// Cooley-Tukey (DIT) butterfly, inputs/outputs in [0, p).
+HK_DEV void ct_bfly(uint32_t &u, uint32_t &v, uint2 w, uint32_t p) {
+    uint32_t t = red1(shoup(v, w.x, w.y, p), p);
+    v = subm(u, t, p);
+    u = addm(u, t, p);
+}
+
+// ------------------------------------------------------------------------------------------
+// Shared-memory NTT over `batch` arrays of N = 2^LOGN points: array b, point i lives at
+// s[b * rs + pad(i)].  Twiddle table tw[h + j] = (omega_{2h}^{+-j}, Shoup quotient) for every
+// half-size h = 1, 2, ..., N/2 and j < h (index 0 unused), read through the read-only path.
+//
+// A radix-2^R pass holds G = 2^R points x[B + j0 + m S] (m < G) of one group in registers and
+// runs R consecutive radix-2 stages on them; S is the smallest half-size of the pass.  Every
+// stage of the pass pairs m with m + 2^l and uses twiddle index h + j0 + S (m mod 2^l),
+// h = S 2^l (the plain radix-2 DIF/DIT indexing, just blocked).
+
+// Forward DIF pass: stages h = S 2^(R-1) ... S.  ZERO_UPPER: the array's upper half is known to
+// be zero (only legal for the first pass, S G = N).
+template <int LOGN, int R, int S, bool ZERO_UPPER>
+HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ tw, uint32_t p,
+                     int tid, int nthr) {
+    constexpr int N = 1 << LOGN;
+    constexpr int G = 1 << R;
+    constexpr int NG = N / G;
+    static_assert(!ZERO_UPPER || S * G == N, "ZERO_UPPER only for the first pass");
+    const int total = batch * NG;
+    for (int gi = tid; gi < total; gi += nthr) {
+        const int b = gi / NG;
+        const int g = gi % NG;
+        const int j0 = g % S;
+        const int B = (g / S) * (S * G);
+        uint32_t *base = s + b * rs;
+        uint32_t v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) {
+            if (ZERO_UPPER && m >= G / 2) v[m] = 0;
+            else v[m] = base[pad(B + j0 + m * S)];
+        }
+#pragma unroll
+        for (int l = R - 1; l >= 0; --l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                const int j = j0 + S * (m & (half - 1));
+                const uint2 w = __ldg(&tw[S * half + j]);
+                gs_bfly(v[m], v[m + half], w, p);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m) base[pad(B + j0 + m * S)] = v[m];
+    }
+    __syncthreads();
+}
+
+// Inverse DIT pass: stages h = S, 2S, ..., S 2^(R-1).
+template <int LOGN, int R, int S>
+HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ tw, uint32_t p,
+                     int tid, int nthr) {
+    constexpr int N = 1 << LOGN;
+    constexpr int G = 1 << R;
+    constexpr int NG = N / G;
+    const int total = batch * NG;
+    for (int gi = tid; gi < total; gi += nthr) {
+        const int b = gi / NG;
+        const int g = gi % NG;
+        const int j0 = g % S;
+        const int B = (g / S) * (S * G);
+        uint32_t *base = s + b * rs;
+        uint32_t v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) v[m] = base[pad(B + j0 + m * S)];
+#pragma unroll
+        for (int l = 0; l < R; ++l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                const int j = j0 + S * (m & (half - 1));
+                const uint2 w = __ldg(&tw[S * half + j]);
+                ct_bfly(v[m], v[m + half], w, p);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m) base[pad(B + j0 + m * S)] = v[m];
+    }
+    __syncthreads();
+}
+
+// Full forward transform: passes of RMAX stages from the top (HI = number of stages left).
+template <int LOGN, int HI, int RMAX, bool FIRST>
+struct DifPasses {
+    static HK_DEV void run(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
+                           int nthr, bool zero_upper) {
+        constexpr int R = HI < RMAX ? HI : RMAX;
+        constexpr int S = 1 << (HI - R);
+        if (FIRST && zero_upper)
+            dif_pass<LOGN, R, S, FIRST>(s, batch, rs, tw, p, tid, nthr);
+        else
+            dif_pass<LOGN, R, S, false>(s, batch, rs, tw, p, tid, nthr);
+        DifPasses<LOGN, HI - R, RMAX, false>::run(s, batch, rs, tw, p, tid, nthr, false);
+    }
+};
+template <int LOGN, int RMAX, bool FIRST>
+struct DifPasses<LOGN, 0, RMAX, FIRST> {
+    static HK_DEV void run(uint32_t *, int, int, const uint2 *, uint32_t, int, int, bool) {}
+};
+
+template <int LOGN, int LO, int RMAX>
+struct DitPasses {
+    static HK_DEV void run(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
+                           int nthr) {
+        constexpr int LEFT = LOGN - LO;
+        constexpr int R = LEFT < RMAX ? LEFT : RMAX;
+        dit_pass<LOGN, R, (1 << LO)>(s, batch, rs, tw, p, tid, nthr);
+        DitPasses<LOGN, LO + R, RMAX>::run(s, batch, rs, tw, p, tid, nthr);
+    }
+};
+template <int LOGN, int RMAX>
+struct DitPasses<LOGN, LOGN, RMAX> {
+    static HK_DEV void run(uint32_t *, int, int, const uint2 *, uint32_t, int, int) {}
+};
+
+template <int LOGN, int RMAX>
+HK_DEV void ntt_forward(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
+                        int nthr, bool zero_upper) {
+    DifPasses<LOGN, LOGN, RMAX, true>::run(s, batch, rs, tw, p, tid, nthr, zero_upper);
+}
+template <int LOGN, int RMAX>
+HK_DEV void ntt_inverse(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
+                        int nthr) {
+    DitPasses<LOGN, 0, RMAX>::run(s, batch, rs, tw, p, tid, nthr);
+}
+
+}  // namespace hk

@@ -1,0 +1,547 @@
+// hk_ntt.cu -- the hot path: exact multiprecision Hankel/Toeplitz/circulant matvec as a 2-D
+// multi-prime NTT convolution.
+//
+//   K0 k0_init           twiddle tables + workspace header (once per plan)
+//   K1 k1_slice_rowntt   A1 limb slicing + validation, A2 slice-dimension forward NTT (N2)
+//   K2 k2_column         A2 matrix-index forward NTTs (N1) of X^ and A^ columns, A3 pointwise
+//                        Montgomery product, inverse matrix-index NTT, keep the n needed rows
+//   K3a k3a_row_intt     A3 inverse slice-dimension NTT per output row
+//   K3b k3b_crt_carry    A3 Garner CRT -> signed coefficients, A4 carry propagation and
+//                        sign-magnitude output
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdio>
+
+#include "hk_internal.h"
+#include "hk_modarith.cuh"
+
+namespace hk {
+
+// ------------------------------------------------------------------------------------------
+// K0: twiddle tables.  Per prime: [N2 fwd | N2 inv | N1 fwd | N1 inv]; entry h + j of a table
+// of length N holds omega_{2h}^{+-j} and its Shoup quotient floor(W 2^32 / p).
+__device__ uint32_t mulmod_slow(uint32_t a, uint32_t b, uint32_t p) {
+    return (uint32_t)(((uint64_t)a * b) % p);
+}
+__device__ uint32_t powmod_slow(uint32_t g, uint64_t e, uint32_t p) {
+    uint32_t r = 1 % p, b = g % p;
+    while (e) {
+        if (e & 1) r = mulmod_slow(r, b, p);
+        b = mulmod_slow(b, b, p);
+        e >>= 1;
+    }
+    return r;
+}
+
+__global__ void k0_init(Params prm, uint2 *tw, uint32_t g0, uint32_t g1, uint32_t g2, uint32_t g3,
+                        uint32_t g4) {
+    const uint32_t gens[kNumPrimes] = {g0, g1, g2, g3, g4};
+    const int N2 = prm.N2, N1 = prm.N1;
+    const int per = 2 * (N2 + N1);
+    const int64_t total = (int64_t)kNumPrimes * per;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int kp = (int)(idx / per);
+        int e = (int)(idx % per);
+        int N, inv;
+        if (e < N2) { N = N2; inv = 0; }
+        else if (e < 2 * N2) { N = N2; inv = 1; e -= N2; }
+        else if (e < 2 * N2 + N1) { N = N1; inv = 0; e -= 2 * N2; }
+        else { N = N1; inv = 1; e -= 2 * N2 + N1; }
+        (void)N;
+        const uint32_t p = prm.pc[kp].p;
+        uint32_t W = 1;
+        if (e > 0) {
+            const int h = 1 << (31 - __clz(e));
+            const int j = e - h;
+            const uint32_t root = powmod_slow(gens[kp], (uint64_t)(p - 1) / (uint64_t)(2 * h), p);
+            W = powmod_slow(root, inv ? (uint64_t)(2 * h - j) : (uint64_t)j, p);
+        }
+        tw[idx] = make_uint2(W, (uint32_t)(((uint64_t)W << 32) / p));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        prm.hdr->magic = kWsMagic;
+        prm.hdr->hash = prm.hash;
+        prm.hdr->status = HK_OK;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K1: slice + residues + slice-dimension forward NTT.  One CTA = 16 entries (rows) of a or x.
+constexpr int kK1Threads = 256;
+constexpr int kTileRows = 16;
+
+template <int LOGN2>
+constexpr int k1_row_stride() { return padded_len(1 << LOGN2) + 1; }
+
+HK_DEV uint32_t digit_residue(uint64_t lo, uint32_t top, const uint32_t *F, const uint32_t *Fq,
+                              uint32_t p) {
+    // (lo mod 2^32) F0 + (lo >> 32) F1 + top F2  (mod p), each Shoup product in [0, 2p)
+    uint32_t r0 = red1(shoup((uint32_t)lo, F[0], Fq[0], p), p);
+    uint32_t r1 = red1(shoup((uint32_t)(lo >> 32), F[1], Fq[1], p), p);
+    uint32_t r = addm(r0, r1, p);
+    if (top) r = addm(r, F[2], p);
+    return r;
+}
+
+template <int LOGN2>
+__global__ void __launch_bounds__(kK1Threads) k1_slice_rowntt(Params prm, int which) {
+    constexpr int N2 = 1 << LOGN2;
+    constexpr int HALF = N2 / 2;
+    constexpr int RS = k1_row_stride<LOGN2>();
+    extern __shared__ uint32_t sm[];
+    __shared__ int8_t s_sign[kTileRows];
+    __shared__ int s_nz[kTileRows];
+
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    if (prm.hdr->magic != kWsMagic || prm.hdr->hash != prm.hash) {
+        if (tid == 0 && blockIdx.x == 0) atomicMin(&prm.hdr->status, (int)HK_EINVAL);
+        return;
+    }
+    const uint64_t *mag = which ? prm.x_mag : prm.a_mag;
+    const int8_t *sgn = which ? prm.x_sign : prm.a_sign;
+    const int64_t count = which ? prm.n : prm.a_count;
+    uint32_t *out = which ? prm.Xhat : prm.Ahat;
+    const int64_t ld = which ? prm.ldX : prm.ldA;
+    const bool rev = which && prm.x_reversed;
+    const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
+    const int L = prm.L, w = prm.w, Ls = prm.Ls;
+
+    // ---- validation (A1): bits >= P zero, sign in {-1,0,1}, sign == 0 <=> magnitude == 0
+    const int rem = prm.P - 64 * (L - 1);
+    const uint64_t topmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
+    if (tid < kTileRows) s_nz[tid] = 0;
+    __syncthreads();
+    bool bad = false;
+    for (int idx = tid; idx < kTileRows * L; idx += nthr) {
+        const int r = idx / L, u = idx - (idx / L) * L;
+        const int64_t row = r0 + r;
+        if (row >= count) continue;
+        const uint64_t v = mag[row * L + u];
+        if (v) s_nz[r] = 1;
+        if (u == L - 1 && (v & ~topmask)) bad = true;
+    }
+    __syncthreads();
+    if (tid < kTileRows) {
+        const int64_t row = r0 + tid;
+        int s = 0;
+        if (row < count) {
+            s = sgn[row];
+            if (s < -1 || s > 1 || ((s == 0) != (s_nz[tid] == 0))) bad = true;
+        }
+        s_sign[tid] = (int8_t)s;
+    }
+    if (bad) atomicMin(&prm.hdr->status, (int)HK_ERANGE);
+    __syncthreads();
+
+    for (int kp = 0; kp < kNumPrimes; ++kp) {
+        const uint32_t p = prm.pc[kp].p;
+        const uint32_t *F = which ? prm.pc[kp].fx : prm.pc[kp].fa;
+        const uint32_t *Fq = which ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
+        // ---- A1: w-bit slices of the magnitude -> signed residues (upper half stays zero)
+        for (int idx = tid; idx < kTileRows * HALF; idx += nthr) {
+            const int r = idx / HALF, t = idx % HALF;
+            const int64_t row = r0 + r;
+            uint32_t res = 0;
+            const int s = s_sign[r];
+            if (t < Ls && s != 0) {
+                const int o = w * t, q = o >> 6, sh = o & 63;
+                const uint64_t *rp = mag + row * L;
+                const uint64_t l0 = rp[q];
+                const uint64_t l1 = (q + 1 < L) ? rp[q + 1] : 0ull;
+                uint64_t lo = sh ? ((l0 >> sh) | (l1 << (64 - sh))) : l0;
+                uint32_t top = 0;
+                if (w < 64) lo &= (1ull << w) - 1;
+                else if (w == 65) top = (uint32_t)((l1 >> sh) & 1ull);
+                res = digit_residue(lo, top, F, Fq, p);
+                if (s < 0 && res) res = p - res;
+            }
+            sm[r * RS + pad(t)] = res;
+        }
+        __syncthreads();
+        // ---- A2 (row pass): forward DIF over the slice index, zero-padded upper half
+        const uint2 *tw = prm.tw + (size_t)kp * 2 * (prm.N2 + prm.N1);
+        ntt_forward<LOGN2, 5>(sm, kTileRows, RS, tw, p, tid, nthr, true);
+        // ---- write [prime][sigma][row] (x rows reversed: matrix index n-1-row)
+        for (int idx = tid; idx < N2 * kTileRows; idx += nthr) {
+            const int sigma = idx / kTileRows, r = idx % kTileRows;
+            const int64_t row = r0 + r;
+            if (row < count) {
+                const int64_t pos = rev ? (count - 1 - row) : row;
+                out[((int64_t)kp * N2 + sigma) * ld + pos] = sm[r * RS + pad(sigma)];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K2: one CTA per (prime, sigma) column: forward NTT of X^ and A^ columns over the matrix
+// index, pointwise Montgomery product (X^ pre-scaled by 2^32 (N1 N2)^-1 in K1), inverse NTT,
+// keep the needed rows.
+template <int LOGN1>
+constexpr int k2_threads() {
+    return (1 << LOGN1) / 32 < 32 ? 32 : ((1 << LOGN1) / 32 > 512 ? 512 : (1 << LOGN1) / 32);
+}
+
+template <int LOGN1>
+__global__ void __launch_bounds__(k2_threads<LOGN1>()) k2_column(Params prm) {
+    constexpr int N1 = 1 << LOGN1;
+    constexpr int T = k2_threads<LOGN1>();
+    constexpr int E = N1 / T;
+    extern __shared__ uint32_t sm[];
+    const int tid = threadIdx.x;
+    const int N2 = prm.N2;
+    const int col = blockIdx.x;
+    const int kp = col >> prm.log_n2;
+    const int sigma = col & (N2 - 1);
+    const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
+    const uint2 *tw = prm.tw + (size_t)kp * 2 * (N2 + N1);
+    const uint2 *twf = tw + 2 * N2, *twi = tw + 2 * N2 + N1;
+    const size_t cidx = (size_t)kp * N2 + sigma;
+
+    // X^ column (x rows already in convolution order), zero-padded to N1
+    {
+        const uint32_t *xc = prm.Xhat + cidx * prm.ldX;
+        const int nx = (int)prm.n;
+        const bool zu = nx <= N1 / 2;
+        const int lim = zu ? N1 / 2 : N1;
+        for (int i = tid; i < lim; i += T) sm[pad(i)] = i < nx ? xc[i] : 0u;
+        __syncthreads();
+        ntt_forward<LOGN1, 5>(sm, 1, 0, twf, p, tid, T, zu);
+    }
+    uint32_t xr[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) xr[e] = sm[pad(tid + e * T)];
+    __syncthreads();
+    {
+        const uint32_t *ac = prm.Ahat + cidx * prm.ldA;
+        const int na = (int)prm.a_count;
+        const bool zu = na <= N1 / 2;
+        const int lim = zu ? N1 / 2 : N1;
+        for (int i = tid; i < lim; i += T) sm[pad(i)] = i < na ? ac[i] : 0u;
+        __syncthreads();
+        ntt_forward<LOGN1, 5>(sm, 1, 0, twf, p, tid, T, zu);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = pad(tid + e * T);
+        sm[i] = mont(sm[i], xr[e], p, pneg);
+    }
+    __syncthreads();
+    ntt_inverse<LOGN1, 5>(sm, 1, 0, twi, p, tid, T);
+    uint32_t *yc = prm.Yhat + cidx * prm.ldY;
+    const int m = (int)prm.m, off = (int)prm.out_off, nn = (int)prm.n;
+    for (int i = tid; i < m; i += T) {
+        uint32_t v = sm[pad(off + i)];
+        if (prm.fold) v = addm(v, sm[pad(off + i + nn)], p);
+        yc[i] = v;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3a: inverse slice-dimension NTT for 16 output rows x one prime.
+template <int LOGN2>
+__global__ void __launch_bounds__(kK1Threads) k3a_row_intt(Params prm) {
+    constexpr int N2 = 1 << LOGN2;
+    constexpr int RS = k1_row_stride<LOGN2>();
+    extern __shared__ uint32_t sm[];
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int kp = blockIdx.y;
+    const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
+    const int64_t m = prm.m;
+    const uint32_t p = prm.pc[kp].p;
+    for (int idx = tid; idx < N2 * kTileRows; idx += nthr) {
+        const int sigma = idx / kTileRows, r = idx % kTileRows;
+        const int64_t row = r0 + r;
+        sm[r * RS + pad(sigma)] =
+            row < m ? prm.Yhat[((int64_t)kp * N2 + sigma) * prm.ldY + row] : 0u;
+    }
+    __syncthreads();
+    const uint2 *twi = prm.tw + (size_t)kp * 2 * (prm.N2 + prm.N1) + N2;
+    ntt_inverse<LOGN2, 5>(sm, kTileRows, RS, twi, p, tid, nthr);
+    const int S2 = prm.S2;
+    for (int idx = tid; idx < kTileRows * S2; idx += nthr) {
+        const int r = idx / S2, t = idx - (idx / S2) * S2;
+        const int64_t row = r0 + r;
+        if (row < m) prm.Yres[(row * kNumPrimes + kp) * prm.ldS + t] = sm[r * RS + pad(t)];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3b: Garner CRT (balanced mixed radix) -> signed coefficient C_s (|C_s| < M/2 < 2^155),
+// Y = sum_s C_s 2^(w s) mod 2^(64 Ly), carry propagation by a block scan of carry-transfer
+// functions, two's complement -> sign-magnitude.
+HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint64_t &c0, uint64_t &c1,
+                   uint64_t &c2) {
+    int32_t v[kNumPrimes];
+#pragma unroll
+    for (int k = 0; k < kNumPrimes; ++k) {
+        const uint32_t p = prm.pc[k].p;
+        uint32_t t = r[k];
+#pragma unroll
+        for (int j = 0; j < k; ++j) {
+            const uint32_t vm = v[j] < 0 ? (uint32_t)(v[j] + (int32_t)p) : (uint32_t)v[j];
+            t = subm(t, vm, p);
+            t = red1(shoup(t, prm.gc.inv[j][k], prm.gc.inv_q[j][k], p), p);
+        }
+        v[k] = t > (p >> 1) ? (int32_t)(t - p) : (int32_t)t;
+    }
+    // C = v0 + p0 (v1 + p1 (v2 + p2 (v3 + p3 v4)))
+    __int128 acc = v[4];
+    acc = acc * (__int128)prm.pc[3].p + v[3];
+    acc = acc * (__int128)prm.pc[2].p + v[2];
+    acc = acc * (__int128)prm.pc[1].p + v[1];  // |acc| < 2^124
+    const uint64_t p0 = prm.pc[0].p;
+    const uint64_t alo = (uint64_t)acc;
+    const __int128 ahi = acc >> 64;                                  // signed, |ahi| < 2^60
+    const __int128 s = (__int128)((unsigned __int128)alo * p0) + v[0];  // in (-2^31, 2^95)
+    const __int128 H = ahi * (__int128)p0 + (s >> 64);
+    c0 = (uint64_t)s;
+    c1 = (uint64_t)H;
+    c2 = (uint64_t)(H >> 64);
+}
+
+// carry-transfer function {-1,0,1} -> {-1,0,1}, packed 2 bits per input (value + 1)
+HK_DEV int tf_apply(int f, int c) { return ((f >> (2 * (c + 1))) & 3) - 1; }
+HK_DEV int tf_compose(int g, int f) {  // g o f
+    int h = 0;
+#pragma unroll
+    for (int c = -1; c <= 1; ++c) h |= (tf_apply(g, tf_apply(f, c)) + 1) << (2 * (c + 1));
+    return h;
+}
+constexpr int kTfId = (0) | (1 << 2) | (2 << 4);
+
+__global__ void __launch_bounds__(kK3Threads) k3b_crt_carry(Params prm) {
+    extern __shared__ uint64_t coef[];  // [S2][3] 192-bit two's complement coefficients
+    __shared__ int64_t s_elast[kK3Threads];
+    __shared__ int s_wtot[kK3Threads / 32];
+    __shared__ int s_wcarry[kK3Threads / 32];
+    __shared__ int s_neg, s_zmin;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t row = blockIdx.x;
+    const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
+
+    for (int s = tid; s < S2; s += kK3Threads) {
+        uint32_t r[kNumPrimes];
+#pragma unroll
+        for (int kp = 0; kp < kNumPrimes; ++kp)
+            r[kp] = prm.Yres[(row * kNumPrimes + kp) * prm.ldS + s];
+        uint64_t c0, c1, c2;
+        garner(r, prm, c0, c1, c2);
+        coef[3 * s] = c0;
+        coef[3 * s + 1] = c1;
+        coef[3 * s + 2] = c2;
+    }
+    if (tid == 0) { s_neg = 0; s_zmin = INT_MAX; }
+    __syncthreads();
+
+    const int chunk = (Ly + kK3Threads - 1) / kK3Threads;
+    const int l0 = tid * chunk;
+    const int l1 = min(Ly, l0 + chunk);
+    uint64_t u[kK3MaxChunk];
+    int64_t e[kK3MaxChunk];
+#pragma unroll
+    for (int c = 0; c < kK3MaxChunk; ++c) {
+        u[c] = 0;
+        e[c] = 0;
+        const int l = l0 + c;
+        if (c < chunk && l < l1) {
+            __int128 acc = 0;
+            const int smin = max(0, (64 * (l - 4) + w - 1) / w);
+            const int smax = min(S2 - 1, (64 * l + 63) / w);
+            for (int s = smin; s <= smax; ++s) {
+                const int o = w * s, q = o >> 6, sh = o & 63, d = l - q;
+                if (d < 0) continue;
+                const uint64_t C0 = coef[3 * s], C1 = coef[3 * s + 1], C2 = coef[3 * s + 2];
+                const bool neg = (int64_t)C2 < 0;
+                if (d <= 3) {
+                    const uint64_t C3 = neg ? ~0ull : 0ull;
+                    const uint64_t Wd = d == 0 ? C0 : d == 1 ? C1 : d == 2 ? C2 : C3;
+                    const uint64_t Wm = d == 0 ? 0ull : d == 1 ? C0 : d == 2 ? C1 : C2;
+                    const uint64_t piece = sh ? ((Wd << sh) | (Wm >> (64 - sh))) : Wd;
+                    acc += (__int128)(unsigned __int128)piece;
+                } else if (d == 4 && neg) {
+                    acc -= 1;
+                }
+            }
+            u[c] = (uint64_t)acc;
+            e[c] = (int64_t)(acc >> 64);
+        }
+    }
+    // carry out of this thread's last limb -> next thread's first limb
+    {
+        int64_t last = 0;
+#pragma unroll
+        for (int c = 0; c < kK3MaxChunk; ++c)
+            if (c < chunk && l0 + c < l1) last = e[c];
+        s_elast[tid] = last;
+    }
+    __syncthreads();
+    // u_l = w_l + e_{l-1}; g_l in {-1,0,1}; transfer f_l(c) = g_l + [u_l+c overflows]
+    int F = kTfId;
+    int fl[kK3MaxChunk];
+    {
+        int64_t ein = tid > 0 ? s_elast[tid - 1] : 0;
+#pragma unroll
+        for (int c = 0; c < kK3MaxChunk; ++c) {
+            fl[c] = kTfId;
+            if (c < chunk && l0 + c < l1) {
+                const uint64_t wv = u[c];
+                const uint64_t uv = wv + (uint64_t)ein;
+                int g = 0;
+                if (ein > 0 && uv < wv) g = 1;
+                if (ein < 0 && uv > wv) g = -1;
+                u[c] = uv;
+                int f = 0;
+#pragma unroll
+                for (int ci = -1; ci <= 1; ++ci) {
+                    const int o = g + ((ci == 1 && uv == ~0ull) ? 1 : 0) - ((ci == -1 && uv == 0) ? 1 : 0);
+                    f |= (o + 1) << (2 * (ci + 1));
+                }
+                fl[c] = f;
+                F = tf_compose(f, F);
+                ein = e[c];
+            }
+        }
+    }
+    // block scan of transfer functions (low limbs first)
+    int incl = F;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int other = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl = tf_compose(incl, other);
+    }
+    if (lane == 31) s_wtot[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        int c = 0;
+        for (int wi = 0; wi < kK3Threads / 32; ++wi) {
+            s_wcarry[wi] = c;
+            c = tf_apply(s_wtot[wi], c);
+        }
+    }
+    __syncthreads();
+    const int prev = __shfl_up_sync(0xffffffffu, incl, 1);
+    int carry = s_wcarry[warp];
+    if (lane > 0) carry = tf_apply(prev, carry);
+    // final limbs (mod 2^(64 Ly))
+    int zloc = INT_MAX;
+#pragma unroll
+    for (int c = 0; c < kK3MaxChunk; ++c) {
+        if (c < chunk && l0 + c < l1) {
+            const uint64_t v = u[c] + (uint64_t)(int64_t)carry;
+            carry = tf_apply(fl[c], carry);
+            u[c] = v;
+            if (v && zloc == INT_MAX) zloc = l0 + c;
+            if (l0 + c == Ly - 1) s_neg = (int)(v >> 63);
+        }
+    }
+    if (zloc != INT_MAX) atomicMin(&s_zmin, zloc);
+    __syncthreads();
+    const bool neg = s_neg != 0;
+    const int zmin = s_zmin;
+    const int64_t orow = prm.reverse_out ? (prm.m - 1 - row) : row;
+    uint64_t *yo = prm.y_mag + orow * Ly;
+#pragma unroll
+    for (int c = 0; c < kK3MaxChunk; ++c) {
+        const int l = l0 + c;
+        if (c < chunk && l < l1) {
+            uint64_t v = u[c];
+            if (neg) v = l < zmin ? 0ull : (l == zmin ? (0ull - v) : ~v);
+            yo[l] = v;
+        }
+    }
+    if (tid == 0) prm.y_sign[orow] = neg ? (int8_t)-1 : (zmin < Ly ? (int8_t)1 : (int8_t)0);
+}
+
+// ------------------------------------------------------------------------------------------
+// launchers
+static int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "hk: CUDA launch error: %s\n", cudaGetErrorString(e));
+        return HK_ECUDA;
+    }
+    return HK_OK;
+}
+
+int launch_init(const Params &prm, const uint32_t *gens, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t total = (int64_t)kNumPrimes * 2 * (prm.N2 + prm.N1);
+    const int threads = 256;
+    const int blocks = (int)((total + threads - 1) / threads);
+    k0_init<<<blocks, threads, 0, st>>>(prm, const_cast<uint2 *>(prm.tw), gens[0], gens[1],
+                                        gens[2], gens[3], gens[4]);
+    return check_launch();
+}
+
+template <int LOGN2>
+static int launch_rows(const Params &prm, cudaStream_t st) {
+    const size_t smem = (size_t)kTileRows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
+    if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    if (cudaFuncSetAttribute(k3a_row_intt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    const int ga = (int)((prm.a_count + kTileRows - 1) / kTileRows);
+    const int gx = (int)((prm.n + kTileRows - 1) / kTileRows);
+    k1_slice_rowntt<LOGN2><<<ga, kK1Threads, smem, st>>>(prm, 0);
+    k1_slice_rowntt<LOGN2><<<gx, kK1Threads, smem, st>>>(prm, 1);
+    return check_launch();
+}
+
+template <int LOGN2>
+static int launch_rows_inverse(const Params &prm, cudaStream_t st) {
+    const size_t smem = (size_t)kTileRows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
+    dim3 grid((unsigned)((prm.m + kTileRows - 1) / kTileRows), kNumPrimes);
+    k3a_row_intt<LOGN2><<<grid, kK1Threads, smem, st>>>(prm);
+    return check_launch();
+}
+
+template <int LOGN1>
+static int launch_cols(const Params &prm, cudaStream_t st) {
+    const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
+    if (cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    k2_column<LOGN1><<<kNumPrimes * prm.N2, k2_threads<LOGN1>(), smem, st>>>(prm);
+    return check_launch();
+}
+
+int launch_ntt_path(const Params &prm, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc;
+    switch (prm.log_n2) {
+#define HK_CASE(LG) case LG: rc = launch_rows<LG>(prm, st); break;
+        HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
+    if (rc) return rc;
+    switch (prm.log_n1) {
+#define HK_CASE(LG) case LG: rc = launch_cols<LG>(prm, st); break;
+        HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12)
+        HK_CASE(13) HK_CASE(14) HK_CASE(15)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
+    if (rc) return rc;
+    switch (prm.log_n2) {
+#define HK_CASE(LG) case LG: rc = launch_rows_inverse<LG>(prm, st); break;
+        HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
+    if (rc) return rc;
+    const size_t smem3 = (size_t)prm.S2 * 3 * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(k3b_crt_carry, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem3) != cudaSuccess)
+        return HK_ECUDA;
+    k3b_crt_carry<<<(unsigned)prm.m, kK3Threads, smem3, st>>>(prm);
+    return check_launch();
+}
+
+}  // namespace hk

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element.
+
+Bit-exact on every output limb and sign (all inputs are integers; reading R10 makes
+the byte image unique).  Full-oracle cases span several tiles and ragged tails; the BASELINE
+configs at full size are checked on sampled rows with the oracle plus modular fingerprints of
+every row (tests/fingerprint.py), in the launch configuration bench.py times."""
+import numpy as np
+import pytest
+
+import hkinputs as gen
+import oracle
+from oracle import bruteforce as bf
+from tests import fingerprint as fp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def hk():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1402_5287_b200 as hk
+    return hk
+
+
+def run_gpu(hk, kind, a_mag, a_sign, x_mag, x_sign, P, m=None, ws=None):
+    am, asg = hk.to_device(a_mag, a_sign)
+    xm, xsg = hk.to_device(x_mag, x_sign)
+    ym, ys = hk.matvec(kind, am, asg, xm, xsg, P, m=m, ws=ws)
+    torch.cuda.synchronize()
+    return hk.to_host(ym, ys)
+
+
+def assert_same(got, want, ctx=""):
+    gm, gs = got
+    wm, ws = want
+    bad = np.nonzero((gm != wm).any(axis=1) | (gs != ws))[0]
+    assert bad.size == 0, f"{ctx}: {bad.size} rows differ, first {bad[:8]}"
+
+
+def full_case(hk, kind, n, P, seed, recipe="uniform", m=None):
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed, recipe, m=m)
+    got = run_gpu(hk, kind, am, asg, xm, xsg, P, m=m)
+    want = oracle.matvec(kind, P, am, asg, xm, xsg, m=m)
+    assert_same(got, want, f"kind={kind} n={n} P={P} m={m}")
+
+
+# ---------------------------------------------------------------------------------------------
+def test_c1_all_kinds(hk):
+    for kind in (0, 1, 2):
+        full_case(hk, kind, 64, 3328, 0)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 17, 33, 100, 257])
+@pytest.mark.parametrize("P", [1, 64, 65, 127, 1000])
+def test_small_edge_sizes(hk, n, P):
+    for kind in (0, 1, 2):
+        full_case(hk, kind, n, P, seed=n * 1000 + P)
+
+
+@pytest.mark.parametrize("n,P", [(300, 5000), (129, 33216), (1000, 700), (64, 16608)])
+def test_medium_full_oracle(hk, n, P):
+    for kind in (0, 1, 2):
+        full_case(hk, kind, n, P, seed=n + P)
+
+
+@pytest.mark.parametrize("n", [64, 128, 512])
+def test_cyclic_circulant_power_of_two(hk, n):
+    assert hk.plan(2, n, 2000)["cyclic"] == 1
+    full_case(hk, 2, n, 2000, seed=n)
+
+
+def test_carry_stress_small(hk):
+    for kind in (1, 2):
+        full_case(hk, kind, 200, 4000, seed=4, recipe="carry_stress")
+
+
+def test_closed_forms(hk):
+    """max magnitude everywhere (largest output) and alternating signs (exact cancellation)."""
+    for n, P in [(7, 3328), (64, 16608), (300, 1000)]:
+        for kind in (0, 1, 2):
+            am, asg = gen.max_magnitude(gen.a_count(kind, n), P)
+            xm, xsg = gen.max_magnitude(n, P)
+            got = run_gpu(hk, kind, am, asg, xm, xsg, P)
+            Mx = (1 << P) - 1
+            want = bf.from_ints([n * Mx * Mx] * n, gen.n_out_limbs(P))
+            assert_same(got, want, f"max n={n} P={P} kind={kind}")
+        am, asg = gen.max_magnitude(2 * n - 1, P)
+        xm, xsg = gen.max_magnitude(n, P, signs=[(-1) ** j for j in range(1, n + 1)])
+        got = run_gpu(hk, 0, am, asg, xm, xsg, P)
+        Mx = (1 << P) - 1
+        want = bf.from_ints([0 if n % 2 == 0 else -Mx * Mx] * n, gen.n_out_limbs(P))
+        assert_same(got, want, f"alternating n={n}")
+
+
+def test_zero_inputs(hk):
+    am, asg = gen.zeros(2 * 50 - 1, 3000)
+    xm, xsg = gen.uniform(1, 1, 50, 3000)
+    gm, gs = run_gpu(hk, 0, am, asg, xm, xsg, 3000)
+    assert not gm.any() and not gs.any()
+
+
+def test_rect_windows(hk):
+    """Row-block shards: m x n windows of a Hankel product."""
+    for (m, n) in [(1, 200), (37, 100), (250, 250), (100, 37)]:
+        full_case(hk, 0, n, 3000, seed=m + n, m=m)
+
+
+def test_host_buffer_path(hk):
+    am, asg, xm, xsg = gen.make_inputs(0, 200, 5000, seed=3)
+    ym, ys = hk.matvec_host(0, am, asg, xm, xsg, 5000)
+    assert_same((ym, ys), oracle.matvec(0, 5000, am, asg, xm, xsg), "host path")
+
+
+def test_workspace_reuse_and_determinism(hk):
+    am, asg, xm, xsg = gen.make_inputs(0, 500, 8000, seed=12)
+    ws = hk.Workspace(0, 500, 8000)
+    r1 = run_gpu(hk, 0, am, asg, xm, xsg, 8000, ws=ws)
+    r2 = run_gpu(hk, 0, am, asg, xm, xsg, 8000, ws=ws)
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+    fp.check(0, am, asg, xm, xsg, *r1)
+
+
+# ---------------------------------------------------------------------------------------------
+# data validation (fault injection)
+def _expect_status(hk, kind, am, asg, xm, xsg, P, code):
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    ws = hk.Workspace(kind, xm.shape[0], P)
+    hk.matvec(kind, a, sa, x, sx, P, ws=ws, check=False)
+    assert ws.status() == code
+
+
+def test_rejects_bits_above_P(hk):
+    P = 100
+    am, asg, xm, xsg = gen.make_inputs(0, 20, P, seed=1)
+    am[5, 1] |= np.uint64(1 << 40)  # bit 104 >= P
+    _expect_status(hk, 0, am, asg, xm, xsg, P, hk.HK_ERANGE)
+
+
+def test_rejects_sign_magnitude_mismatch(hk):
+    P = 200
+    am, asg, xm, xsg = gen.make_inputs(0, 20, P, seed=2)
+    xsg = xsg.copy(); xm = xm.copy()
+    xm[3] = 0; xsg[3] = 1  # zero magnitude with sign +1
+    _expect_status(hk, 0, am, asg, xm, xsg, P, hk.HK_ERANGE)
+    am, asg, xm, xsg = gen.make_inputs(0, 20, P, seed=2)
+    asg = asg.copy(); asg[7] = 2
+    _expect_status(hk, 0, am, asg, xm, xsg, P, hk.HK_ERANGE)
+    am, asg, xm, xsg = gen.make_inputs(0, 20, P, seed=2)
+    asg = asg.copy(); asg[0] = 0  # non-zero magnitude with sign 0
+    _expect_status(hk, 0, am, asg, xm, xsg, P, hk.HK_ERANGE)
+
+
+def test_uninitialised_workspace(hk):
+    P = 128
+    am, asg, xm, xsg = gen.make_inputs(0, 10, P, seed=3)
+    ws = hk.Workspace(0, 11, P)  # initialised for n = 11, used for n = 10 -> rejected by binding
+    with pytest.raises(ValueError):
+        hk.matvec(0, *hk.to_device(am, asg), *hk.to_device(xm, xsg), P, ws=ws)
+    # a zeroed buffer passed through the raw ABI -> device-side EINVAL
+    nbytes = hk.workspace_size(0, 10, P)
+    buf = torch.zeros(nbytes + 256, dtype=torch.uint8, device="cuda")
+    ptr = (buf.data_ptr() + 255) & ~255
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    y = torch.empty((10, gen.n_out_limbs(P)), dtype=torch.int64, device="cuda")
+    ysg = torch.empty(10, dtype=torch.int8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    rc = hk._lib.hk_hankel_matvec(10, P, a.data_ptr(), sa.data_ptr(), x.data_ptr(), sx.data_ptr(),
+                                  y.data_ptr(), ysg.data_ptr(), ptr, nbytes, s)
+    assert rc == hk.HK_OK
+    import ctypes
+    v = ctypes.c_int32()
+    assert hk._lib.hk_workspace_status(ptr, s, ctypes.byref(v)) == 0
+    assert v.value == hk.HK_EINVAL
+
+
+def test_undersized_workspace_and_overlap(hk):
+    P = 128
+    am, asg, xm, xsg = gen.make_inputs(0, 10, P, seed=3)
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    ws = hk.Workspace(0, 10, P)
+    s = torch.cuda.current_stream().cuda_stream
+    y = torch.empty((10, gen.n_out_limbs(P)), dtype=torch.int64, device="cuda")
+    ysg = torch.empty(10, dtype=torch.int8, device="cuda")
+    rc = hk._lib.hk_hankel_matvec(10, P, a.data_ptr(), sa.data_ptr(), x.data_ptr(), sx.data_ptr(),
+                                  y.data_ptr(), ysg.data_ptr(), ws.ptr, ws.nbytes - 1024, s)
+    assert rc == hk.HK_ENOMEM
+    rc = hk._lib.hk_hankel_matvec(10, P, a.data_ptr(), sa.data_ptr(), x.data_ptr(), sx.data_ptr(),
+                                  a.data_ptr(), ysg.data_ptr(), ws.ptr, ws.nbytes, s)
+    assert rc == hk.HK_EINVAL
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE configs at full size (sampled rows + fingerprints of every row)
+SAMPLE_ROWS = 12
+
+
+def _sampled(hk, name, rows_extra=()):
+    c = gen.CONFIGS[name]
+    kind, n, P = c["kind"], c["n"], c["P"]
+    am, asg, xm, xsg = gen.config_inputs(name)
+    gm, gs = run_gpu(hk, kind, am, asg, xm, xsg, P)
+    fp.check(kind, am, asg, xm, xsg, gm, gs)
+    rng = np.random.default_rng(123)
+    rows = np.unique(np.concatenate([np.array([0, 1, n // 2, n - 2, n - 1], dtype=np.int64),
+                                     rng.integers(0, n, SAMPLE_ROWS).astype(np.int64),
+                                     np.asarray(rows_extra, dtype=np.int64)]))
+    wm, ws_ = oracle.matvec(kind, P, am, asg, xm, xsg, rows=rows)
+    assert_same((gm[rows], gs[rows]), (wm, ws_), f"{name} sampled rows")
+
+
+def test_c2_full_oracle(hk):
+    c = gen.CONFIGS["C2"]
+    am, asg, xm, xsg = gen.config_inputs("C2")
+    got = run_gpu(hk, 0, am, asg, xm, xsg, c["P"])
+    fp.check(0, am, asg, xm, xsg, *got)
+    rows = np.arange(0, 1024, 16)
+    wm, ws_ = oracle.matvec(0, c["P"], am, asg, xm, xsg, rows=rows)
+    assert_same((got[0][rows], got[1][rows]), (wm, ws_), "C2 rows")
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5T", "C5C"])
+def test_config_sampled(hk, name):
+    _sampled(hk, name)
+
+
+# ---------------------------------------------------------------------------------------------
+# companion A6: schoolbook kernel
+@pytest.mark.parametrize("n,P", [(1, 64), (5, 65), (64, 3328), (100, 1000), (33, 16608)])
+def test_schoolbook_parity(hk, n, P):
+    for kind in (0, 1, 2):
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=n + 7)
+        a, sa = hk.to_device(am, asg)
+        x, sx = hk.to_device(xm, xsg)
+        ym, ys = hk.schoolbook_matvec(kind, a, sa, x, sx, P)
+        torch.cuda.synchronize()
+        assert_same(hk.to_host(ym, ys), oracle.matvec(kind, P, am, asg, xm, xsg),
+                    f"schoolbook kind={kind} n={n} P={P}")

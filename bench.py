@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- exact multiprecision Hankel matvec throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {hk,reference}] [--config C3]
+
+A step is one full matvec (all SURVEY.md 8(a) rows A1-A4: slicing, 2-D forward NTT, pointwise,
+inverse NTT, CRT, carry) over the BASELINE workload, with inputs resident in HBM.  N = 1 runs
+C3 (Hankel n = 8000, P = 33,216 bits, seed 2).  N > 1 (torchrun, NCCL) runs the row-block plan
+of paper_1402_5287_b200.dist: each rank computes its nr x n Hankel window with the CUDA path and
+the y rows are all-gathered; value = matvecs/s of the whole job, time = max over ranks.
+
+--impl reference times the oracle (plain C schoolbook, oracle/) on the host cores on a bounded
+sample of output rows of the same workload (all rows cost the same n L^2 limb products).
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import hkinputs as gen  # noqa: E402
+
+METRIC = "Hankel matvecs/sec at n=8000, P=33,216 bits"
+UNIT = "matvec/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT_B200 = 148
+LANES_PER_SM = 128  # 4 SMSPs x 32 lanes: issue limit of integer instructions per clock
+# algorithmic SASS instructions per operation of the number system
+I_GS, I_CT, I_MONT = 7, 8, 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hk", choices=["hk", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(gen.CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+def workload(cfg_name):
+    c = gen.CONFIGS[cfg_name]
+    kind = c["kind"]
+    return dict(name=cfg_name, kind=kind, n=c["n"], P=c["P"], seed=c["seed"], recipe=c["recipe"],
+                desc=f"{cfg_name} {gen.KIND_NAMES[kind]} n={c['n']} P={c['P']} seed={c['seed']} "
+                     f"{c['recipe']}")
+
+
+def alg_counts(plan, m=None):
+    """Algorithmic operation counts per matvec: full transforms, no
+    pruning credit."""
+    k = plan["k_primes"]
+    N1, N2 = 1 << plan["log_n1"], 1 << plan["log_n2"]
+    lg1, lg2 = plan["log_n1"], plan["log_n2"]
+    rows_a, n = plan["a_count"], plan["n"]
+    m = plan["m"] if m is None else m
+    bf_row_fwd = k * (rows_a + n) * (N2 // 2) * lg2
+    bf_col_fwd = k * N2 * 2 * (N1 // 2) * lg1
+    bf_col_inv = k * N2 * (N1 // 2) * lg1
+    bf_row_inv = k * m * (N2 // 2) * lg2
+    pointwise = k * N2 * N1
+    k2_instr = I_GS * bf_col_fwd + I_CT * bf_col_inv + I_MONT * pointwise
+    return dict(bf_row_fwd=bf_row_fwd, bf_col_fwd=bf_col_fwd, bf_col_inv=bf_col_inv,
+                bf_row_inv=bf_row_inv, pointwise=pointwise, k2_instr=k2_instr,
+                butterflies=bf_row_fwd + bf_col_fwd + bf_col_inv + bf_row_inv)
+
+
+def alg_bytes(plan):
+    """Algorithmic HBM bytes per matvec: a, x, y once + one write and one read of each
+    transform-domain array (A^, X^ row pass outputs, Y^ column pass output)."""
+    L, Ly, k = plan["L"], plan["Ly"], plan["k_primes"]
+    N2 = 1 << plan["log_n2"]
+    io = (plan["a_count"] + plan["n"]) * (8 * L + 1) + plan["m"] * (8 * Ly + 1)
+    inter = 2 * 4 * k * N2 * (plan["a_count"] + plan["n"] + plan["m"])
+    return io, io + inter
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = []
+        for ts, line in self.samples:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 7:
+                continue
+            try:
+                rows.append((ts, float(parts[0]), float(parts[1]), parts[3:]))
+            except ValueError:
+                continue
+        inside = [r for r in rows if t0 - 0.05 <= r[0] <= t1 + 0.05]
+        use = inside if inside else rows[-5:]
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in use for i, v in enumerate(r[3]) if v.startswith("Active")})
+        return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": max(r[2] for r in use),
+                "reasons": reasons, "samples": len(use), "in_timed_region": bool(inside)}
+
+
+def cpu_baseline(wl, rows_per_thread=1):
+    """The oracle as it stands, on a bounded sample of output rows, all host cores."""
+    import oracle
+    kind, n, P = wl["kind"], wl["n"], wl["P"]
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, wl["seed"], wl["recipe"])
+    cores = oracle.default_threads()
+    R = min(n, cores * rows_per_thread)
+    rows = np.linspace(0, n - 1, R).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.matvec(kind, P, am, asg, xm, xsg, rows=rows, threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": (R / n) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{R} of {n} output rows of {wl['name']} (each row = n*L^2 = "
+                      f"{n * gen.n_limbs(P) ** 2:.3g} limb products), {dt:.2f} s, extrapolated "
+                      f"to whole matvecs"}
+
+
+# ---------------------------------------------------------------------------------------------
+def run_reference(args, wl, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    oracle.build_oracle()
+    vals = []
+    t_all = time.perf_counter()
+    cb = None
+    budget_s = float(os.environ.get("HK_REFERENCE_BUDGET_S", "240"))
+    steps_run = 0
+    for _ in range(args.steps):  # each step: one row per host thread (bounded sample)
+        cb = cpu_baseline(wl)
+        vals.append(cb["value"])
+        steps_run += 1
+        if time.perf_counter() - t_all > budget_s:
+            break
+    value = statistics.median(vals)
+    ms = 1000.0 / value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps_run, "steps_requested": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl["desc"]},
+            "cpu_baseline": {**cb, "value": value},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_all}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    wl = workload(args.config)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, wl, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_1402_5287_b200 as hk
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    kind, n, P = wl["kind"], wl["n"], wl["P"]
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, wl["seed"], wl["recipe"])
+    a, sa = hk.to_device(am, asg, dev)
+    x, sx = hk.to_device(xm, xsg, dev)
+    stream = torch.cuda.current_stream()
+
+    plan = hk.plan(kind, n, P)
+    W, K = max(3, args.warmup), args.steps
+    stage_names = ("K1_slice_rowntt", "K2_column", "K3_finish")
+    if world == 1:
+        prob = hk.Problem(kind, a, sa, x, sx, P)
+        prob.run()
+        if prob.status() != hk.HK_OK:
+            raise SystemExit("bench: device status not OK")
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+
+        def step(i=None):
+            if i is None:
+                prob.run()
+                return
+            e = ev[i]
+            e[0].record(stream)
+            prob.run(hk.STAGE_SLICE_ROWS)
+            e[1].record(stream)
+            prob.run(hk.STAGE_COLUMNS)
+            e[2].record(stream)
+            prob.run(hk.STAGE_FINISH)
+            e[3].record(stream)
+        launches_per_step = 5  # K1 (a), K1 (x), K2, K3a, K3b
+    else:
+        from paper_1402_5287_b200 import dist as hkdist
+        sh = hkdist.ShardedHankel(a, sa, x, sx, P)
+        sh.step()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+
+        def step(i=None):
+            if i is None:
+                sh.step()
+                return
+            e = ev[i]
+            e[0].record(stream)
+            e[1].record(stream)
+            if sh.nr > 0:
+                sh.compute(sh.win[0], sh.win[1], sh.x[0], sh.x[1], P, sh.nr,
+                           out=(sh.y_loc[: sh.nr], sh.s_loc[: sh.nr]), ws=sh.ws)
+            e[2].record(stream)
+            sh._gather()
+            e[3].record(stream)
+        launches_per_step = 5
+
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        time.sleep(0.3)
+    # ---- timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    t_start.record(stream)
+    for i in range(K):
+        step(i)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall1 = time.time()
+    ms_total = t_start.elapsed_time(t_end)
+    if world > 1:
+        tt = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_total = float(tt.item())
+    ms_step = ms_total / K
+    stage_ms = [statistics.mean(ev[i][s].elapsed_time(ev[i][s + 1]) for i in range(K))
+                for s in range(3)]
+    clocks = sampler.summary(wall0, wall1) if sampler else None
+    if sampler:
+        sampler.stop()
+
+    # ---- e2e through the host-buffer C-ABI call (N = 1 workload per rank)
+    e2e = None
+    if rank == 0 and not args.no_e2e and world == 1:
+        pa = torch.from_numpy(am.view(np.int64)).pin_memory()
+        ps = torch.from_numpy(asg).pin_memory()
+        px = torch.from_numpy(xm.view(np.int64)).pin_memory()
+        pxs = torch.from_numpy(xsg).pin_memory()
+        Ly = plan["Ly"]
+        py = torch.empty((n, Ly), dtype=torch.int64).pin_memory()
+        pys = torch.empty((n,), dtype=torch.int8).pin_memory()
+        wsh = hk.Workspace(kind, n, P, flags=hk.WS_STAGING)
+        for _ in range(2):
+            hk.matvec_host(kind, pa, ps, px, pxs, P, out=(py, pys), ws=wsh)
+        Ke = max(3, min(K, 20))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(Ke):
+            hk.matvec_host(kind, pa, ps, px, pxs, P, out=(py, pys), ws=wsh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / Ke
+        h2d = am.nbytes + asg.nbytes + xm.nbytes + xsg.nbytes
+        d2h = n * Ly * 8 + n + 4
+        e2e = {"value": 1000.0 / ms_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": ms_e2e, "steps": Ke}
+        del wsh
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (K2 column pass): ALU issue bound
+    cnt = alg_counts(plan)
+    peaks = {}
+    if os.path.exists(PEAKS_FILE):
+        peaks = json.load(open(PEAKS_FILE))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tinstr = nsm * LANES_PER_SM * sm_max * 1e6 / 1e12
+    k2_ms = stage_ms[1]
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "k2_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(wl["name"])
+        except (ValueError, OSError):
+            traffic = None
+    achieved = cnt["k2_instr"] / (k2_ms * 1e-3) / 1e12 if world == 1 else None
+    io_bytes, all_bytes = alg_bytes(plan)
+    roof = {"bound": "alu", "kernel": "k2_column", "achieved": achieved, "peak": peak_tinstr,
+            "unit": "Tinstr/s", "frac": (achieved / peak_tinstr) if achieved else None,
+            "traffic": traffic,
+            "peak_source": f"derived: {nsm} SMs x {LANES_PER_SM} int32 lanes x {sm_max:.0f} MHz "
+                           f"(B200_PROFILING.md clocks; MEASURED_PEAKS.json sm_max_mhz)",
+            "algorithmic_per_launch": cnt["k2_instr"],
+            "per_unit": f"{I_GS}/GS butterfly, {I_CT}/CT butterfly, {I_MONT}/pointwise product",
+            "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms_step}
+    hbm_peak = float(peaks.get("hbm_gbs", 6549.4))
+    roof["hbm_check"] = {"alg_bytes_per_step": all_bytes,
+                         "achieved_gbs": all_bytes / (ms_step * 1e-3) / 1e9, "peak_gbs": hbm_peak}
+
+    cb = None
+    if not args.no_cpu:
+        cb = cpu_baseline(wl)
+
+    value = 1000.0 / ms_step  # one matvec per step for the whole job
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded SplitMix64 mantissas, BASELINE configs recipe)",
+        "config": {"workload": wl["desc"], "kind": gen.KIND_NAMES[kind], "n": n, "P": P,
+                   "plan": {k: plan[k] for k in ("w", "Ls", "log_n1", "log_n2", "k_primes",
+                                                 "margin_bits")},
+                   "parallelism": "single GPU" if world == 1 else f"row-block x{world} + NCCL all-gather",
+                   "l2": "no flush: per-step working set (inputs 100 MB + transform-domain "
+                         f"{all_bytes / 1e6:.0f} MB traffic) exceeds the 126 MB L2"},
+        "stages_ms": dict(zip(stage_names if world == 1 else ("-", "shard_compute", "all_gather"),
+                              stage_ms)),
+        "roofline": roof,
+        "cpu_baseline": cb,
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * K,
+        "clocks": clocks,
+        "library": hk.library_path(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -162,6 +162,25 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P,
                        uint64_t *y_mag_host, int8_t *y_sign_host,
                        void *ws, size_t ws_bytes, void *stream);
 
+/* Pipeline stages of the NTT path, for per-kernel timing (bench.py) and phase-wise use:
+ *   HK_STAGE_SLICE_ROWS  K1: validation, slicing, slice-dimension forward NTT of a and x
+ *   HK_STAGE_COLUMNS     K2: matrix-index forward NTTs, pointwise product, inverse NTT
+ *   HK_STAGE_FINISH      K3: inverse slice-dimension NTT, CRT, carry, sign-magnitude y
+ * hk_matvec_stages runs the selected stages, in this order, with exactly the launches the
+ * matvec entry points make; a stage reads what the previous stage left in ws, so running
+ * HK_STAGE_COLUMNS or HK_STAGE_FINISH without the earlier stages of the same inputs gives an
+ * unspecified y.  The data-status word is reset when HK_STAGE_SLICE_ROWS is selected.
+ * Arguments as hk_matvec_host but DEVICE pointers. */
+#define HK_STAGE_SLICE_ROWS 1u
+#define HK_STAGE_COLUMNS 2u
+#define HK_STAGE_FINISH 4u
+#define HK_STAGE_ALL 7u
+int32_t hk_matvec_stages(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t stages,
+                         const uint64_t *a_mag, const int8_t *a_sign,
+                         const uint64_t *x_mag, const int8_t *x_sign,
+                         uint64_t *y_mag, int8_t *y_sign,
+                         void *ws, size_t ws_bytes, void *stream);
+
 /* Companion A6: direct schoolbook limb-product matvec on the GPU, no
  * transform: y_i = sum_j A_{idx(i,j)} X_j with 32-bit limb products and wide column sums.
  * kind / m / n / shapes as above (HK_HANKEL with m < n = rectangular window).  Needs no

@@ -64,6 +64,8 @@ def _load():
         "hk_hankel_rect_matvec": (i32, [i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_host": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_schoolbook_matvec": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
+        "hk_matvec_stages": (i32, [i32, i64, i64, i32, ctypes.c_uint32, vp, vp, vp, vp, vp, vp,
+                                   vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -76,7 +78,8 @@ _lib = _load()
 EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_workspace_size",
             "hk_workspace_init", "hk_workspace_status", "hk_hankel_matvec", "hk_toeplitz_matvec",
             "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host",
-            "hk_schoolbook_matvec")
+            "hk_schoolbook_matvec", "hk_matvec_stages")
+STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
 def library_path() -> str:
@@ -242,6 +245,36 @@ def matvec_host(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None
                              hptr(out[0]), hptr(out[1]), ws.ptr, ws.nbytes, _stream_ptr(stream))
     _check(rc, "hk_matvec_host")
     return out
+
+
+class Problem:
+    """A prepared device problem (inputs, output and workspace resident in HBM) for repeated
+    calls; ``run(stages)`` launches the selected pipeline stages on the current stream."""
+
+    def __init__(self, kind, a_mag, a_sign, x_mag, x_sign, P, m=None, stream=None):
+        import torch
+        self.kind, self.P = int(kind), int(P)
+        self.n = int(x_mag.shape[0])
+        self.m = self.n if m is None else int(m)
+        L, Ly = limbs(P), out_limbs(P)
+        na = (self.n if kind == CIRCULANT else self.m + self.n - 1)
+        self.inputs = (a_mag, a_sign, x_mag, x_sign)
+        self.ptrs = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+                     _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+                     _dev_ptr(x_mag, _mag_dtypes(), (self.n, L), "x_mag"),
+                     _dev_ptr(x_sign, (torch.int8,), (self.n,), "x_sign")]
+        self.y_mag = torch.empty((self.m, Ly), dtype=a_mag.dtype, device=a_mag.device)
+        self.y_sign = torch.empty((self.m,), dtype=torch.int8, device=a_mag.device)
+        self.ptrs += [self.y_mag.data_ptr(), self.y_sign.data_ptr()]
+        self.ws = Workspace(kind, self.n, P, m=self.m, stream=stream)
+
+    def run(self, stages: int = STAGE_ALL, stream=None) -> None:
+        rc = _lib.hk_matvec_stages(self.kind, self.m, self.n, self.P, stages, *self.ptrs,
+                                   self.ws.ptr, self.ws.nbytes, _stream_ptr(stream))
+        _check(rc, "hk_matvec_stages")
+
+    def status(self, stream=None) -> int:
+        return self.ws.status(stream)
 
 
 def schoolbook_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, stream=None):

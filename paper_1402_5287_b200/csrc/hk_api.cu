@@ -241,7 +241,8 @@ bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
 
 int run_matvec(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
-               uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+               uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream,
+               uint32_t stages = HK_STAGE_ALL) {
     if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws) return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, 0, &pl);
@@ -261,9 +262,10 @@ int run_matvec(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_
     fill_params(pl, ws, &prm);
     prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
     prm.y_mag = y_mag; prm.y_sign = y_sign;
-    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+    if ((stages & HK_STAGE_SLICE_ROWS) &&
+        cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
         return HK_ECUDA;
-    return launch_ntt_path(prm, stream);
+    return launch_ntt_path(prm, stream, stages);
 }
 
 }  // namespace
@@ -397,6 +399,15 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
     rc = hk_workspace_status(ws, stream, &ds);
     if (rc) return rc;
     return ds;
+}
+
+int32_t hk_matvec_stages(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t stages,
+                         const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
+                         const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *ws,
+                         size_t ws_bytes, void *stream) {
+    if (stages == 0 || (stages & ~HK_STAGE_ALL)) return HK_EINVAL;
+    return run_matvec(kind, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws, ws_bytes,
+                      stream, stages);
 }
 
 int32_t hk_schoolbook_matvec(int32_t kind, int64_t m, int64_t n, int32_t P,

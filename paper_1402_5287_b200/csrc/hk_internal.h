@@ -74,7 +74,7 @@ struct Plan {
 
 // kernels (hk_ntt.cu)
 int launch_init(const Params &prm, const uint32_t *gens, void *stream);
-int launch_ntt_path(const Params &prm, void *stream);
+int launch_ntt_path(const Params &prm, void *stream, uint32_t stages);
 // companion (hk_schoolbook.cu)
 int launch_schoolbook(int kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                       const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,

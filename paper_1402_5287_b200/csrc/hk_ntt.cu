@@ -511,17 +511,17 @@ static int launch_cols(const Params &prm, cudaStream_t st) {
     return check_launch();
 }
 
-int launch_ntt_path(const Params &prm, void *stream) {
+int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
     cudaStream_t st = (cudaStream_t)stream;
-    int rc;
-    switch (prm.log_n2) {
+    int rc = HK_OK;
+    if (stages & HK_STAGE_SLICE_ROWS) switch (prm.log_n2) {
 #define HK_CASE(LG) case LG: rc = launch_rows<LG>(prm, st); break;
         HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)
 #undef HK_CASE
         default: return HK_EUNSUPPORTED;
     }
     if (rc) return rc;
-    switch (prm.log_n1) {
+    if (stages & HK_STAGE_COLUMNS) switch (prm.log_n1) {
 #define HK_CASE(LG) case LG: rc = launch_cols<LG>(prm, st); break;
         HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12)
         HK_CASE(13) HK_CASE(14) HK_CASE(15)
@@ -529,6 +529,7 @@ int launch_ntt_path(const Params &prm, void *stream) {
         default: return HK_EUNSUPPORTED;
     }
     if (rc) return rc;
+    if (!(stages & HK_STAGE_FINISH)) return HK_OK;
     switch (prm.log_n2) {
 #define HK_CASE(LG) case LG: rc = launch_rows_inverse<LG>(prm, st); break;
         HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)

@@ -1,0 +1,106 @@
+"""Multi-GPU Hankel matvec: row-block sharding with an all-gather of y (BASELINE north_star;
+SURVEY.md 8(e) plan P-3).
+
+One process per GPU (torchrun), torch.distributed for the plumbing (NCCL over NVLink on GPUs,
+gloo in the CPU tests).  Rank g owns output rows [r0, r0 + nr) of the n x n Hankel product; its
+shard is itself a Hankel product -- the nr x n window over a[r0 .. r0 + nr + n - 2] (PAPER.md
+P:50-60: row i only touches a_i .. a_{i+n-1}) -- computed by the C-ABI CUDA path
+(hk_hankel_rect_matvec).  The y rows are then all-gathered so every rank holds the full y.
+There is no other data-path exchange.
+
+The per-shard compute is a parameter so the sharding / gather logic can be exercised on CPU
+(gloo) with any exact shard function; the default is the CUDA path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def row_blocks(n: int, G: int) -> list[tuple[int, int]]:
+    """Balanced contiguous row blocks (r0, nr) for G ranks; the first n % G get one extra row."""
+    if G < 1 or n < 1:
+        raise ValueError("need n >= 1 and G >= 1")
+    base, extra = divmod(n, G)
+    out, r0 = [], 0
+    for g in range(G):
+        nr = base + (1 if g < extra else 0)
+        out.append((r0, nr))
+        r0 += nr
+    return out
+
+
+def window(a_mag, a_sign, r0: int, nr: int, n: int):
+    """Entries a[r0 .. r0 + nr + n - 2] (0-based) feeding output rows r0 .. r0 + nr - 1."""
+    return a_mag[r0:r0 + nr + n - 1], a_sign[r0:r0 + nr + n - 1]
+
+
+def _cuda_shard(a_mag, a_sign, x_mag, x_sign, P, m, out=None, ws=None):
+    from . import hankel_rect_matvec
+    return hankel_rect_matvec(a_mag, a_sign, x_mag, x_sign, P, m, out=out, ws=ws, check=False)
+
+
+class ShardedHankel:
+    """Prepared sharded problem for repeated steps (bench): owns this rank's window, its
+    workspace, the local y block and the gathered y."""
+
+    def __init__(self, a_mag, a_sign, x_mag, x_sign, P, group=None, compute=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.G = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = int(x_mag.shape[0])
+        self.P = int(P)
+        self.blocks = row_blocks(self.n, self.G)
+        self.r0, self.nr = self.blocks[self.rank]
+        self.nr_max = max(nr for _, nr in self.blocks)
+        self.win = window(a_mag, a_sign, self.r0, self.nr, self.n)
+        self.x = (x_mag, x_sign)
+        self.compute = compute or _cuda_shard
+        Ly = 2 * ((P + 63) // 64) + 1
+        dev = a_mag.device
+        self.ws = None
+        if compute is None and self.nr > 0:
+            from . import Workspace, HANKEL
+            self.ws = Workspace(HANKEL, self.n, self.P, m=self.nr)
+        # local block padded to nr_max rows so every rank contributes an equal-size chunk
+        self.y_loc = torch.zeros((self.nr_max, Ly), dtype=a_mag.dtype, device=dev)
+        self.s_loc = torch.zeros((self.nr_max,), dtype=torch.int8, device=dev)
+        self.y_all = torch.empty((self.G * self.nr_max, Ly), dtype=a_mag.dtype, device=dev)
+        self.s_all = torch.empty((self.G * self.nr_max,), dtype=torch.int8, device=dev)
+
+    def step(self):
+        if self.nr > 0:
+            kw = {"ws": self.ws} if self.ws is not None else {}
+            out = (self.y_loc[: self.nr], self.s_loc[: self.nr])
+            ym, ys = self.compute(self.win[0], self.win[1], self.x[0], self.x[1], self.P, self.nr,
+                                  out=out, **kw)
+            if ym.data_ptr() != self.y_loc.data_ptr():
+                self.y_loc[: self.nr].copy_(ym)
+                self.s_loc[: self.nr].copy_(ys)
+        self._gather()
+        return self.result()
+
+    def _gather(self):
+        d = self.dist
+        try:
+            d.all_gather_into_tensor(self.y_all, self.y_loc, group=self.group)
+            d.all_gather_into_tensor(self.s_all, self.s_loc, group=self.group)
+        except (RuntimeError, NotImplementedError, AttributeError):  # backends without _allgather_base
+            ys = list(self.y_all.chunk(self.G))
+            ss = list(self.s_all.chunk(self.G))
+            d.all_gather(ys, self.y_loc, group=self.group)
+            d.all_gather(ss, self.s_loc, group=self.group)
+
+    def result(self):
+        """Full y (n rows) in row order, from the gathered padded blocks."""
+        import torch
+        idx = np.concatenate([np.arange(g * self.nr_max, g * self.nr_max + nr)
+                              for g, (_, nr) in enumerate(self.blocks)])
+        it = torch.from_numpy(idx).to(self.y_all.device)
+        return self.y_all.index_select(0, it), self.s_all.index_select(0, it)
+
+
+def hankel_matvec(a_mag, a_sign, x_mag, x_sign, P, group=None, compute=None):
+    """y = A_H x sharded by rows over the process group; returns the full y on every rank."""
+    return ShardedHankel(a_mag, a_sign, x_mag, x_sign, P, group=group, compute=compute).step()

@@ -1,0 +1,83 @@
+"""Multi-process (world_size 2, gloo, CPU) test of the row-block sharding + all-gather path of
+paper_1402_5287_b200.dist.  The per-shard compute is the oracle here (tests may call it); on
+GPUs the same ShardedHankel runs the CUDA shard kernel over NCCL."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import hkinputs as gen
+import oracle
+from paper_1402_5287_b200 import dist as hkdist
+
+
+def test_row_blocks_cover_rows_exactly():
+    for n in (1, 2, 7, 8000, 16384):
+        for G in (1, 2, 3, 4, 8):
+            b = hkdist.row_blocks(n, G)
+            assert len(b) == G and sum(nr for _, nr in b) == n
+            assert all(b[i][0] + b[i][1] == b[i + 1][0] for i in range(G - 1))
+            assert max(nr for _, nr in b) - min(nr for _, nr in b) <= 1
+
+
+def test_window_is_a_hankel_shard():
+    """Rows r0..r0+nr-1 of the n x n Hankel product == the nr x n window product."""
+    P, n = 300, 11
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=5)
+    full = oracle.matvec(0, P, am, asg, xm, xsg, threads=2)
+    for r0, nr in hkdist.row_blocks(n, 3):
+        wm, ws = hkdist.window(am, asg, r0, nr, n)
+        part = oracle.matvec(0, P, wm, ws, xm, xsg, m=nr, threads=2)
+        assert np.array_equal(part[0], full[0][r0:r0 + nr])
+        assert np.array_equal(part[1], full[1][r0:r0 + nr])
+
+
+def _oracle_shard(a_mag, a_sign, x_mag, x_sign, P, m, out=None):
+    ym, ys = oracle.matvec(0, P, a_mag.numpy().view(np.uint64), a_sign.numpy(),
+                           x_mag.numpy().view(np.uint64), x_sign.numpy(), m=m, threads=1)
+    return torch.from_numpy(ym.view(np.int64)), torch.from_numpy(ys)
+
+
+def _worker(rank, world, port, n, P, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=17)
+        t = [torch.from_numpy(am.view(np.int64)), torch.from_numpy(asg),
+             torch.from_numpy(xm.view(np.int64)), torch.from_numpy(xsg)]
+        ym, ys = hkdist.hankel_matvec(*t, P, compute=_oracle_shard)
+        q.put((rank, ym.numpy().view(np.uint64).copy(), ys.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("n", [9, 16])
+def test_sharded_matvec_gloo_world2(n):
+    P = 400
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, P, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=17)
+    wm, ws = oracle.matvec(0, P, am, asg, xm, xsg, threads=2)
+    for _, ym, ys in res:
+        assert np.array_equal(ym, wm) and np.array_equal(ys, ws)

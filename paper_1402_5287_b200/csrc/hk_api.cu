@@ -151,7 +151,7 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     const int64_t N1 = int64_t(1) << in.log_n1;
     size_t off = align256(sizeof(WsHeader));
     pl->off_tw = off;
-    off = align256(off + (size_t)kNumPrimes * 2 * (N1 + N2) * sizeof(uint2));
+    off = align256(off + (size_t)kNumPrimes * (N1 + N2) * sizeof(uint2));
     pl->off_A = off;
     size_t szA = (size_t)kNumPrimes * N2 * pl->ldA * 4;
     const size_t szRes = (size_t)m * kNumPrimes * pl->ldS * 4;  // Yres aliases A^

@@ -57,7 +57,7 @@ struct Params {
     int8_t *y_sign;
     // workspace regions
     WsHeader *hdr;
-    const uint2 *tw;             // per prime: [N2 fwd | N2 inv | N1 fwd | N1 inv]
+    const uint2 *tw;             // per prime: [N2 forward table | N1 forward table]
     uint32_t *Ahat, *Xhat, *Yhat, *Yres;
     PrimeConsts pc[kNumPrimes];
     GarnerConsts gc;

@@ -1,0 +1,215 @@
+// hk_k2.cuh -- K2, the matrix-index (column) pass of the 2-D NTT convolution (SURVEY.md 8(a)
+// rows A2/A3).  One CTA handles one (prime, sigma) column of N1 = 2^LOGN points:
+//
+//   X^ : first DIF pass straight from HBM -> middle passes in smem -> last pass kept in registers
+//   A^ : first DIF pass straight from HBM -> middle passes -> last pass in registers,
+//        pointwise Montgomery product with the held X^ values, first DIT pass (same groups) in
+//        registers -> middle DIT passes -> last DIT pass stored straight to Y^ in HBM
+//
+// Pass plan: forward passes of radix 2^5 from the top; the last (S = 1) pass takes the remainder
+// RL = LOGN - 5 (NP - 1).  The inverse mirrors it (RL first, then radix-2^5 passes).  The DIT
+// runs with the FORWARD roots, which yields the inverse transform with the output index negated
+// (hk_modarith.cuh), so output row i is read from position (N1 - out_off - i) mod N1.
+#pragma once
+#include "hk_internal.h"
+#include "hk_modarith.cuh"
+
+namespace hk {
+
+template <int LOGN1>
+constexpr int k2_threads() {
+    return (1 << LOGN1) / 32 < 32 ? 32 : ((1 << LOGN1) / 32 > 512 ? 512 : (1 << LOGN1) / 32);
+}
+
+template <int LOGN>
+struct ColPlan {
+    static constexpr int NP = (LOGN + 4) / 5;         // passes per transform (>= 2 for LOGN >= 6)
+    static constexpr int RL = LOGN - 5 * (NP - 1);    // log2 radix of the bottom pass
+    static constexpr int T = k2_threads<LOGN>();
+    static constexpr int GL = 1 << RL;                // points per bottom-pass group
+    static constexpr int GPT = (1 << LOGN) / GL / T;  // bottom-pass groups per thread
+    static_assert(NP >= 2, "column transforms need LOGN >= 6");
+    static_assert(GPT >= 1 && GPT * GL * T == (1 << LOGN), "bottom pass must tile the threads");
+};
+
+// Top forward pass (R = 5, S = N/32, single block) reading the column straight from HBM.
+template <class TW, int LOGN, int T>
+HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, bool zu,
+                                   uint32_t *sm, const uint2 *tw, uint32_t p) {
+    constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
+    for (int j0 = threadIdx.x; j0 < S; j0 += T) {
+        uint32_t v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) {
+            const int idx = j0 + m * S;
+            v[m] = (!(zu && m >= G / 2) && idx < nsrc) ? __ldcs(src + idx) : 0u;
+        }
+#pragma unroll
+        for (int l = R - 1; l >= 0; --l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                const uint2 w = TW::ld(tw, S * half + j0 + S * (m & (half - 1)));
+                gs_bfly(v[m], v[m + half], w, p);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m) sm[pad(j0 + m * S)] = v[m];
+    }
+    __syncthreads();
+}
+
+// Middle forward passes (R = 5), k = 1 .. NP-2.
+template <class TW, int LOGN, int K>
+struct K2DifMiddle {
+    static HK_DEV void run(uint32_t *sm, const uint2 *tw, uint32_t p) {
+        constexpr int NP = ColPlan<LOGN>::NP;
+        if constexpr (K <= NP - 2) {
+            constexpr int S = 1 << (LOGN - 5 * (K + 1));
+            dif_pass<TW, LOGN, 5, S, false>(sm, 1, 0, tw, p, threadIdx.x, ColPlan<LOGN>::T);
+            K2DifMiddle<TW, LOGN, K + 1>::run(sm, tw, p);
+        }
+    }
+};
+
+// Middle inverse passes (R = 5), from S = 2^RL upwards, all but the top one.
+template <class TW, int LOGN, int LO>
+struct K2DitMiddle {
+    static HK_DEV void run(uint32_t *sm, const uint2 *tw, uint32_t p) {
+        if constexpr (LO + 5 < LOGN) {
+            dit_pass<TW, LOGN, 5, (1 << LO)>(sm, 1, 0, tw, p, threadIdx.x, ColPlan<LOGN>::T);
+            K2DitMiddle<TW, LOGN, LO + 5>::run(sm, tw, p);
+        }
+    }
+};
+
+// Bottom DIF pass (S = 1) of group g held in v[].
+template <class TW, int RL>
+HK_DEV void dif_bottom_regs(uint32_t (&v)[1 << RL], const uint2 *tw, uint32_t p) {
+#pragma unroll
+    for (int l = RL - 1; l >= 0; --l) {
+        const int half = 1 << l;
+#pragma unroll
+        for (int m = 0; m < (1 << RL); ++m) {
+            if (m & half) continue;
+            gs_bfly(v[m], v[m + half], TW::ld(tw, half + (m & (half - 1))), p);
+        }
+    }
+}
+template <class TW, int RL>
+HK_DEV void dit_bottom_regs(uint32_t (&v)[1 << RL], const uint2 *tw, uint32_t p) {
+#pragma unroll
+    for (int l = 0; l < RL; ++l) {
+        const int half = 1 << l;
+#pragma unroll
+        for (int m = 0; m < (1 << RL); ++m) {
+            if (m & half) continue;
+            ct_bfly(v[m], v[m + half], TW::ld(tw, half + (m & (half - 1))), p);
+        }
+    }
+}
+
+// Top inverse pass (R = 5, S = N/32) with the result going to HBM (or back to smem for fold).
+template <class TW, int LOGN, int T>
+HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, uint32_t *__restrict__ yc,
+                       int mrows, int off, bool to_smem) {
+    constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
+    for (int j0 = threadIdx.x; j0 < S; j0 += T) {
+        uint32_t v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) v[m] = sm[pad(j0 + m * S)];
+#pragma unroll
+        for (int l = 0; l < R; ++l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                const uint2 w = TW::ld(tw, S * half + j0 + S * (m & (half - 1)));
+                ct_bfly(v[m], v[m + half], w, p);
+            }
+        }
+        if (to_smem) {
+#pragma unroll
+            for (int m = 0; m < G; ++m) sm[pad(j0 + m * S)] = v[m];
+        } else {
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                const int i = (N - (j0 + m * S) - off) & (N - 1);  // output row of this position
+                if (i < mrows) __stcs(yc + i, v[m]);
+            }
+        }
+    }
+    __syncthreads();
+}
+
+template <class TW, int LOGN1>
+HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
+    using PL = ColPlan<LOGN1>;
+    constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
+    const int tid = threadIdx.x;
+    const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
+    const size_t cidx = (size_t)kp * prm.N2 + sigma;
+
+    // ---- X^: forward, bottom pass kept in registers
+    {
+        const int nx = (int)prm.n;
+        k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx, nx <= N1 / 2, sm, twf, p);
+        K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
+    }
+    uint32_t xr[GPT][GL];
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+        const int g = tid + k * T;
+#pragma unroll
+        for (int m = 0; m < GL; ++m) xr[k][m] = sm[pad(g * GL + m)];
+        dif_bottom_regs<TW, RL>(xr[k], twf, p);
+    }
+    __syncthreads();
+    // ---- A^: forward; bottom pass + pointwise + first inverse pass in registers
+    {
+        const int na = (int)prm.a_count;
+        k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm, twf, p);
+        K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
+    }
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+        const int g = tid + k * T;
+        uint32_t v[GL];
+#pragma unroll
+        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL + m)];
+        dif_bottom_regs<TW, RL>(v, twf, p);
+#pragma unroll
+        for (int m = 0; m < GL; ++m) v[m] = mont(v[m], xr[k][m], p, pneg);
+        dit_bottom_regs<TW, RL>(v, twf, p);
+#pragma unroll
+        for (int m = 0; m < GL; ++m) sm[pad(g * GL + m)] = v[m];
+    }
+    __syncthreads();
+    K2DitMiddle<TW, LOGN1, RL>::run(sm, twf, p);
+    uint32_t *yc = prm.Yhat + cidx * prm.ldY;
+    const int mrows = (int)prm.m, off = (int)prm.out_off;
+    if (!prm.fold) {
+        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, false);
+    } else {  // circulant via linear convolution: y[i] = z[i] + z[i + n]
+        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, true);
+        const int nn = (int)prm.n;
+        for (int i = tid; i < mrows; i += T) {
+            const uint32_t v = sm[pad((N1 - (off + i)) & (N1 - 1))];
+            yc[i] = addm(v, sm[pad((N1 - (off + i + nn)) & (N1 - 1))], p);
+        }
+        __syncthreads();
+    }
+}
+
+// One CTA per column; the N1 forward table is read through the read-only/L1 path.
+template <int LOGN1>
+__global__ void __launch_bounds__(k2_threads<LOGN1>(), 1) k2_column(Params prm) {
+    extern __shared__ uint32_t sm[];
+    const int col = blockIdx.x;
+    const int kp = col >> prm.log_n2;
+    const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1) + prm.N2;
+    k2_column_body<TwGlobal, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
+}
+
+}  // namespace hk

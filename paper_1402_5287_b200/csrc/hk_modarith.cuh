@@ -60,6 +60,14 @@ HK_DEV void ct_bfly(uint32_t &u, uint32_t &v, uint2 w, uint32_t p) {
     u = addm(u, t, p);
 }
 
+// Twiddle-load policies: the table lives in global memory (read-only path) or shared memory.
+struct TwGlobal {
+    static HK_DEV uint2 ld(const uint2 *t, int i) { return __ldg(t + i); }
+};
+struct TwShared {
+    static HK_DEV uint2 ld(const uint2 *t, int i) { return t[i]; }
+};
+
 // ------------------------------------------------------------------------------------------
 // Shared-memory NTT over `batch` arrays of N = 2^LOGN points: array b, point i lives at
 // s[b * rs + pad(i)].  Twiddle table tw[h + j] = (omega_{2h}^{+-j}, Shoup quotient) for every
@@ -69,10 +77,14 @@ HK_DEV void ct_bfly(uint32_t &u, uint32_t &v, uint2 w, uint32_t p) {
 // runs R consecutive radix-2 stages on them; S is the smallest half-size of the pass.  Every
 // stage of the pass pairs m with m + 2^l and uses twiddle index h + j0 + S (m mod 2^l),
 // h = S 2^l (the plain radix-2 DIF/DIT indexing, just blocked).
+//
+// Only FORWARD tables are used.  The DIT network run with the forward roots computes the
+// forward DFT of its bit-reversed input; applied to DIF(x) it returns N * x[(-i) mod N], i.e. the
+// inverse transform with the output index negated -- callers read position (N - i) mod N.
 
 // Forward DIF pass: stages h = S 2^(R-1) ... S.  ZERO_UPPER: the array's upper half is known to
 // be zero (only legal for the first pass, S G = N).
-template <int LOGN, int R, int S, bool ZERO_UPPER>
+template <class TW, int LOGN, int R, int S, bool ZERO_UPPER>
 HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ tw, uint32_t p,
                      int tid, int nthr) {
     constexpr int N = 1 << LOGN;
@@ -99,7 +111,7 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
             for (int m = 0; m < G; ++m) {
                 if (m & half) continue;
                 const int j = j0 + S * (m & (half - 1));
-                const uint2 w = __ldg(&tw[S * half + j]);
+                const uint2 w = TW::ld(tw, S * half + j);
                 gs_bfly(v[m], v[m + half], w, p);
             }
         }
@@ -110,7 +122,7 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
 }
 
 // Inverse DIT pass: stages h = S, 2S, ..., S 2^(R-1).
-template <int LOGN, int R, int S>
+template <class TW, int LOGN, int R, int S>
 HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ tw, uint32_t p,
                      int tid, int nthr) {
     constexpr int N = 1 << LOGN;
@@ -133,7 +145,7 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
             for (int m = 0; m < G; ++m) {
                 if (m & half) continue;
                 const int j = j0 + S * (m & (half - 1));
-                const uint2 w = __ldg(&tw[S * half + j]);
+                const uint2 w = TW::ld(tw, S * half + j);
                 ct_bfly(v[m], v[m + half], w, p);
             }
         }
@@ -144,48 +156,50 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
 }
 
 // Full forward transform: passes of RMAX stages from the top (HI = number of stages left).
-template <int LOGN, int HI, int RMAX, bool FIRST>
+template <class TW, int LOGN, int HI, int RMAX, bool FIRST>
 struct DifPasses {
     static HK_DEV void run(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
                            int nthr, bool zero_upper) {
         constexpr int R = HI < RMAX ? HI : RMAX;
         constexpr int S = 1 << (HI - R);
         if (FIRST && zero_upper)
-            dif_pass<LOGN, R, S, FIRST>(s, batch, rs, tw, p, tid, nthr);
+            dif_pass<TW, LOGN, R, S, FIRST>(s, batch, rs, tw, p, tid, nthr);
         else
-            dif_pass<LOGN, R, S, false>(s, batch, rs, tw, p, tid, nthr);
-        DifPasses<LOGN, HI - R, RMAX, false>::run(s, batch, rs, tw, p, tid, nthr, false);
+            dif_pass<TW, LOGN, R, S, false>(s, batch, rs, tw, p, tid, nthr);
+        DifPasses<TW, LOGN, HI - R, RMAX, false>::run(s, batch, rs, tw, p, tid, nthr, false);
     }
 };
-template <int LOGN, int RMAX, bool FIRST>
-struct DifPasses<LOGN, 0, RMAX, FIRST> {
+template <class TW, int LOGN, int RMAX, bool FIRST>
+struct DifPasses<TW, LOGN, 0, RMAX, FIRST> {
     static HK_DEV void run(uint32_t *, int, int, const uint2 *, uint32_t, int, int, bool) {}
 };
 
-template <int LOGN, int LO, int RMAX>
+template <class TW, int LOGN, int LO, int RMAX>
 struct DitPasses {
     static HK_DEV void run(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
                            int nthr) {
         constexpr int LEFT = LOGN - LO;
         constexpr int R = LEFT < RMAX ? LEFT : RMAX;
-        dit_pass<LOGN, R, (1 << LO)>(s, batch, rs, tw, p, tid, nthr);
-        DitPasses<LOGN, LO + R, RMAX>::run(s, batch, rs, tw, p, tid, nthr);
+        dit_pass<TW, LOGN, R, (1 << LO)>(s, batch, rs, tw, p, tid, nthr);
+        DitPasses<TW, LOGN, LO + R, RMAX>::run(s, batch, rs, tw, p, tid, nthr);
     }
 };
-template <int LOGN, int RMAX>
-struct DitPasses<LOGN, LOGN, RMAX> {
+template <class TW, int LOGN, int RMAX>
+struct DitPasses<TW, LOGN, LOGN, RMAX> {
     static HK_DEV void run(uint32_t *, int, int, const uint2 *, uint32_t, int, int) {}
 };
 
-template <int LOGN, int RMAX>
+// Forward DIF (natural -> bit-reversed).
+template <class TW, int LOGN, int RMAX>
 HK_DEV void ntt_forward(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
                         int nthr, bool zero_upper) {
-    DifPasses<LOGN, LOGN, RMAX, true>::run(s, batch, rs, tw, p, tid, nthr, zero_upper);
+    DifPasses<TW, LOGN, LOGN, RMAX, true>::run(s, batch, rs, tw, p, tid, nthr, zero_upper);
 }
-template <int LOGN, int RMAX>
-HK_DEV void ntt_inverse(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p, int tid,
-                        int nthr) {
-    DitPasses<LOGN, 0, RMAX>::run(s, batch, rs, tw, p, tid, nthr);
+// DIT with the forward table (bit-reversed -> natural, output index negated; see above).
+template <class TW, int LOGN, int RMAX>
+HK_DEV void ntt_dit_fwdroots(uint32_t *s, int batch, int rs, const uint2 *tw, uint32_t p,
+                             int tid, int nthr) {
+    DitPasses<TW, LOGN, 0, RMAX>::run(s, batch, rs, tw, p, tid, nthr);
 }
 
 }  // namespace hk

@@ -15,12 +15,13 @@
 
 #include "hk_internal.h"
 #include "hk_modarith.cuh"
+#include "hk_k2.cuh"
 
 namespace hk {
 
 // ------------------------------------------------------------------------------------------
-// K0: twiddle tables.  Per prime: [N2 fwd | N2 inv | N1 fwd | N1 inv]; entry h + j of a table
-// of length N holds omega_{2h}^{+-j} and its Shoup quotient floor(W 2^32 / p).
+// K0: twiddle tables.  Per prime: [N2 table | N1 table]; entry h + j of a table of length N
+// holds omega_{2h}^j and its Shoup quotient floor(W 2^32 / p) (forward roots only).
 __device__ uint32_t mulmod_slow(uint32_t a, uint32_t b, uint32_t p) {
     return (uint32_t)(((uint64_t)a * b) % p);
 }
@@ -38,25 +39,20 @@ __global__ void k0_init(Params prm, uint2 *tw, uint32_t g0, uint32_t g1, uint32_
                         uint32_t g4) {
     const uint32_t gens[kNumPrimes] = {g0, g1, g2, g3, g4};
     const int N2 = prm.N2, N1 = prm.N1;
-    const int per = 2 * (N2 + N1);
+    const int per = N2 + N1;
     const int64_t total = (int64_t)kNumPrimes * per;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int kp = (int)(idx / per);
         int e = (int)(idx % per);
-        int N, inv;
-        if (e < N2) { N = N2; inv = 0; }
-        else if (e < 2 * N2) { N = N2; inv = 1; e -= N2; }
-        else if (e < 2 * N2 + N1) { N = N1; inv = 0; e -= 2 * N2; }
-        else { N = N1; inv = 1; e -= 2 * N2 + N1; }
-        (void)N;
+        if (e >= N2) e -= N2;  // [N2 table | N1 table], both forward
         const uint32_t p = prm.pc[kp].p;
         uint32_t W = 1;
         if (e > 0) {
             const int h = 1 << (31 - __clz(e));
             const int j = e - h;
             const uint32_t root = powmod_slow(gens[kp], (uint64_t)(p - 1) / (uint64_t)(2 * h), p);
-            W = powmod_slow(root, inv ? (uint64_t)(2 * h - j) : (uint64_t)j, p);
+            W = powmod_slow(root, (uint64_t)j, p);
         }
         tw[idx] = make_uint2(W, (uint32_t)(((uint64_t)W << 32) / p));
     }
@@ -161,8 +157,8 @@ __global__ void __launch_bounds__(kK1Threads) k1_slice_rowntt(Params prm, int wh
         }
         __syncthreads();
         // ---- A2 (row pass): forward DIF over the slice index, zero-padded upper half
-        const uint2 *tw = prm.tw + (size_t)kp * 2 * (prm.N2 + prm.N1);
-        ntt_forward<LOGN2, 5>(sm, kTileRows, RS, tw, p, tid, nthr, true);
+        const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
+        ntt_forward<TwGlobal, LOGN2, 5>(sm, kTileRows, RS, tw, p, tid, nthr, true);
         // ---- write [prime][sigma][row] (x rows reversed: matrix index n-1-row)
         for (int idx = tid; idx < N2 * kTileRows; idx += nthr) {
             const int sigma = idx / kTileRows, r = idx % kTileRows;
@@ -173,70 +169,6 @@ __global__ void __launch_bounds__(kK1Threads) k1_slice_rowntt(Params prm, int wh
             }
         }
         __syncthreads();
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// K2: one CTA per (prime, sigma) column: forward NTT of X^ and A^ columns over the matrix
-// index, pointwise Montgomery product (X^ pre-scaled by 2^32 (N1 N2)^-1 in K1), inverse NTT,
-// keep the needed rows.
-template <int LOGN1>
-constexpr int k2_threads() {
-    return (1 << LOGN1) / 32 < 32 ? 32 : ((1 << LOGN1) / 32 > 512 ? 512 : (1 << LOGN1) / 32);
-}
-
-template <int LOGN1>
-__global__ void __launch_bounds__(k2_threads<LOGN1>()) k2_column(Params prm) {
-    constexpr int N1 = 1 << LOGN1;
-    constexpr int T = k2_threads<LOGN1>();
-    constexpr int E = N1 / T;
-    extern __shared__ uint32_t sm[];
-    const int tid = threadIdx.x;
-    const int N2 = prm.N2;
-    const int col = blockIdx.x;
-    const int kp = col >> prm.log_n2;
-    const int sigma = col & (N2 - 1);
-    const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
-    const uint2 *tw = prm.tw + (size_t)kp * 2 * (N2 + N1);
-    const uint2 *twf = tw + 2 * N2, *twi = tw + 2 * N2 + N1;
-    const size_t cidx = (size_t)kp * N2 + sigma;
-
-    // X^ column (x rows already in convolution order), zero-padded to N1
-    {
-        const uint32_t *xc = prm.Xhat + cidx * prm.ldX;
-        const int nx = (int)prm.n;
-        const bool zu = nx <= N1 / 2;
-        const int lim = zu ? N1 / 2 : N1;
-        for (int i = tid; i < lim; i += T) sm[pad(i)] = i < nx ? xc[i] : 0u;
-        __syncthreads();
-        ntt_forward<LOGN1, 5>(sm, 1, 0, twf, p, tid, T, zu);
-    }
-    uint32_t xr[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) xr[e] = sm[pad(tid + e * T)];
-    __syncthreads();
-    {
-        const uint32_t *ac = prm.Ahat + cidx * prm.ldA;
-        const int na = (int)prm.a_count;
-        const bool zu = na <= N1 / 2;
-        const int lim = zu ? N1 / 2 : N1;
-        for (int i = tid; i < lim; i += T) sm[pad(i)] = i < na ? ac[i] : 0u;
-        __syncthreads();
-        ntt_forward<LOGN1, 5>(sm, 1, 0, twf, p, tid, T, zu);
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int i = pad(tid + e * T);
-        sm[i] = mont(sm[i], xr[e], p, pneg);
-    }
-    __syncthreads();
-    ntt_inverse<LOGN1, 5>(sm, 1, 0, twi, p, tid, T);
-    uint32_t *yc = prm.Yhat + cidx * prm.ldY;
-    const int m = (int)prm.m, off = (int)prm.out_off, nn = (int)prm.n;
-    for (int i = tid; i < m; i += T) {
-        uint32_t v = sm[pad(off + i)];
-        if (prm.fold) v = addm(v, sm[pad(off + i + nn)], p);
-        yc[i] = v;
     }
 }
 
@@ -259,13 +191,14 @@ __global__ void __launch_bounds__(kK1Threads) k3a_row_intt(Params prm) {
             row < m ? prm.Yhat[((int64_t)kp * N2 + sigma) * prm.ldY + row] : 0u;
     }
     __syncthreads();
-    const uint2 *twi = prm.tw + (size_t)kp * 2 * (prm.N2 + prm.N1) + N2;
-    ntt_inverse<LOGN2, 5>(sm, kTileRows, RS, twi, p, tid, nthr);
+    const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
+    ntt_dit_fwdroots<TwGlobal, LOGN2, 5>(sm, kTileRows, RS, twf, p, tid, nthr);
     const int S2 = prm.S2;
     for (int idx = tid; idx < kTileRows * S2; idx += nthr) {
         const int r = idx / S2, t = idx - (idx / S2) * S2;
         const int64_t row = r0 + r;
-        if (row < m) prm.Yres[(row * kNumPrimes + kp) * prm.ldS + t] = sm[r * RS + pad(t)];
+        if (row < m)  // slice index negated (forward-root DIT)
+            prm.Yres[(row * kNumPrimes + kp) * prm.ldS + t] = sm[r * RS + pad((N2 - t) & (N2 - 1))];
     }
 }
 
@@ -469,7 +402,7 @@ static int check_launch() {
 
 int launch_init(const Params &prm, const uint32_t *gens, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t total = (int64_t)kNumPrimes * 2 * (prm.N2 + prm.N1);
+    const int64_t total = (int64_t)kNumPrimes * (prm.N2 + prm.N1);
     const int threads = 256;
     const int blocks = (int)((total + threads - 1) / threads);
     k0_init<<<blocks, threads, 0, st>>>(prm, const_cast<uint2 *>(prm.tw), gens[0], gens[1],
@@ -496,6 +429,9 @@ static int launch_rows(const Params &prm, cudaStream_t st) {
 template <int LOGN2>
 static int launch_rows_inverse(const Params &prm, cudaStream_t st) {
     const size_t smem = (size_t)kTileRows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
+    if (cudaFuncSetAttribute(k3a_row_intt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return HK_ECUDA;
     dim3 grid((unsigned)((prm.m + kTileRows - 1) / kTileRows), kNumPrimes);
     k3a_row_intt<LOGN2><<<grid, kK1Threads, smem, st>>>(prm);
     return check_launch();
@@ -503,11 +439,12 @@ static int launch_rows_inverse(const Params &prm, cudaStream_t st) {
 
 template <int LOGN1>
 static int launch_cols(const Params &prm, cudaStream_t st) {
+    const int ncols = kNumPrimes * prm.N2;
     const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
     if (cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
-    k2_column<LOGN1><<<kNumPrimes * prm.N2, k2_threads<LOGN1>(), smem, st>>>(prm);
+    k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
 }
 

@@ -2,7 +2,8 @@
 // multi-prime NTT convolution.
 //
 //   K0 k0_init           twiddle tables + workspace header (once per plan)
-//   K1 k1_slice_rowntt   A1 limb slicing + validation, A2 slice-dimension forward NTT (N2)
+//   K1 k1_slice_rowntt   A1 limb slicing + validation, A2 slice-dimension forward NTT (N2),
+//                        a and x tiles in one launch
 //   K2 k2_column         A2 matrix-index forward NTTs (N1) of X^ and A^ columns, A3 pointwise
 //                        Montgomery product, inverse matrix-index NTT, keep the n needed rows
 //   K3a k3a_row_intt     A3 inverse slice-dimension NTT per output row
@@ -81,91 +82,140 @@ HK_DEV uint32_t digit_residue(uint64_t lo, uint32_t top, const uint32_t *F, cons
     return r;
 }
 
+// K1 v2: a CTA owns kK1Rows entries (a and x tiles in one launch).  Each thread extracts the
+// w-bit digits of its top-pass group once (registers), then for every prime: residues -> top
+// DIF pass (radix 2^5, upper half zero) in registers -> smem -> remaining passes -> transposed
+// write of [prime][sigma][row] (kK1Rows consecutive rows per sigma = one 32-byte sector).
+constexpr int kK1Rows = 8;
 template <int LOGN2>
-__global__ void __launch_bounds__(kK1Threads) k1_slice_rowntt(Params prm, int which) {
-    constexpr int N2 = 1 << LOGN2;
-    constexpr int HALF = N2 / 2;
-    constexpr int RS = k1_row_stride<LOGN2>();
-    extern __shared__ uint32_t sm[];
-    __shared__ int8_t s_sign[kTileRows];
-    __shared__ int s_nz[kTileRows];
+constexpr int k1_threads() {
+    return kK1Rows * ((1 << LOGN2) / 32 > 8 ? (1 << LOGN2) / 32 : 8);
+}
 
-    const int tid = threadIdx.x, nthr = blockDim.x;
+template <int LOGN2>
+__global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params prm, int tiles_a) {
+    constexpr int N2 = 1 << LOGN2;
+    constexpr int RS = k1_row_stride<LOGN2>();
+    constexpr int T = k1_threads<LOGN2>();
+    constexpr int R1 = 5, G1 = 32, H1 = 16;  // top pass: 32 points, upper 16 are zero padding
+    constexpr int S1 = N2 / G1;              // top-pass groups per row
+    constexpr int TPR = T / kK1Rows;         // threads per row (>= S1)
+    static_assert(LOGN2 >= 5 && TPR >= S1, "K1 tiling");
+    extern __shared__ uint32_t sm[];
+    __shared__ int8_t s_sign[kK1Rows];
+    __shared__ int s_nz[kK1Rows];
+
+    const int tid = threadIdx.x;
     if (prm.hdr->magic != kWsMagic || prm.hdr->hash != prm.hash) {
         if (tid == 0 && blockIdx.x == 0) atomicMin(&prm.hdr->status, (int)HK_EINVAL);
         return;
     }
-    const uint64_t *mag = which ? prm.x_mag : prm.a_mag;
-    const int8_t *sgn = which ? prm.x_sign : prm.a_sign;
-    const int64_t count = which ? prm.n : prm.a_count;
-    uint32_t *out = which ? prm.Xhat : prm.Ahat;
-    const int64_t ld = which ? prm.ldX : prm.ldA;
-    const bool rev = which && prm.x_reversed;
-    const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
+    const bool is_x = (int)blockIdx.x >= tiles_a;
+    const int tile = is_x ? (int)blockIdx.x - tiles_a : (int)blockIdx.x;
+    const uint64_t *mag = is_x ? prm.x_mag : prm.a_mag;
+    const int8_t *sgn = is_x ? prm.x_sign : prm.a_sign;
+    const int64_t count = is_x ? prm.n : prm.a_count;
+    uint32_t *out = is_x ? prm.Xhat : prm.Ahat;
+    const int64_t ld = is_x ? prm.ldX : prm.ldA;
+    const bool rev = is_x && prm.x_reversed;
+    const int64_t r0 = (int64_t)tile * kK1Rows;
     const int L = prm.L, w = prm.w, Ls = prm.Ls;
 
     // ---- validation (A1): bits >= P zero, sign in {-1,0,1}, sign == 0 <=> magnitude == 0
     const int rem = prm.P - 64 * (L - 1);
     const uint64_t topmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
-    if (tid < kTileRows) s_nz[tid] = 0;
+    if (tid < kK1Rows) s_nz[tid] = 0;
     __syncthreads();
     bool bad = false;
-    for (int idx = tid; idx < kTileRows * L; idx += nthr) {
+    for (int idx = tid; idx < kK1Rows * L; idx += T) {
         const int r = idx / L, u = idx - (idx / L) * L;
         const int64_t row = r0 + r;
         if (row >= count) continue;
-        const uint64_t v = mag[row * L + u];
+        const uint64_t v = __ldg(mag + row * L + u);
         if (v) s_nz[r] = 1;
         if (u == L - 1 && (v & ~topmask)) bad = true;
     }
     __syncthreads();
-    if (tid < kTileRows) {
+    if (tid < kK1Rows) {
         const int64_t row = r0 + tid;
-        int s = 0;
+        int sg = 0;
         if (row < count) {
-            s = sgn[row];
-            if (s < -1 || s > 1 || ((s == 0) != (s_nz[tid] == 0))) bad = true;
+            sg = sgn[row];
+            if (sg < -1 || sg > 1 || ((sg == 0) != (s_nz[tid] == 0))) bad = true;
         }
-        s_sign[tid] = (int8_t)s;
+        s_sign[tid] = (int8_t)sg;
     }
     if (bad) atomicMin(&prm.hdr->status, (int)HK_ERANGE);
     __syncthreads();
 
+    // ---- A1: this thread's digits t = j0 + m S1 (m < 16), extracted once for all primes
+    const int r = tid / TPR, j0 = tid % TPR;
+    const int64_t row = r0 + r;
+    const int sg = s_sign[r];
+    const bool act = j0 < S1;
+    uint32_t dlo[H1], dhi[H1], dtop = 0;
+#pragma unroll
+    for (int m = 0; m < H1; ++m) {
+        const int t = j0 + m * S1;
+        uint64_t lo = 0;
+        if (act && sg != 0 && t < Ls) {
+            const int o = w * t, q = o >> 6, sh = o & 63;
+            const uint64_t *rp = mag + row * L;
+            const uint64_t l0 = __ldg(rp + q);
+            const uint64_t l1 = (q + 1 < L) ? __ldg(rp + q + 1) : 0ull;
+            lo = sh ? ((l0 >> sh) | (l1 << (64 - sh))) : l0;
+            if (w < 64) lo &= (1ull << w) - 1;
+            else if (w == 65) dtop |= (uint32_t)((l1 >> sh) & 1ull) << m;
+        }
+        dlo[m] = (uint32_t)lo;
+        dhi[m] = (uint32_t)(lo >> 32);
+    }
+
     for (int kp = 0; kp < kNumPrimes; ++kp) {
         const uint32_t p = prm.pc[kp].p;
-        const uint32_t *F = which ? prm.pc[kp].fx : prm.pc[kp].fa;
-        const uint32_t *Fq = which ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
-        // ---- A1: w-bit slices of the magnitude -> signed residues (upper half stays zero)
-        for (int idx = tid; idx < kTileRows * HALF; idx += nthr) {
-            const int r = idx / HALF, t = idx % HALF;
-            const int64_t row = r0 + r;
-            uint32_t res = 0;
-            const int s = s_sign[r];
-            if (t < Ls && s != 0) {
-                const int o = w * t, q = o >> 6, sh = o & 63;
-                const uint64_t *rp = mag + row * L;
-                const uint64_t l0 = rp[q];
-                const uint64_t l1 = (q + 1 < L) ? rp[q + 1] : 0ull;
-                uint64_t lo = sh ? ((l0 >> sh) | (l1 << (64 - sh))) : l0;
-                uint32_t top = 0;
-                if (w < 64) lo &= (1ull << w) - 1;
-                else if (w == 65) top = (uint32_t)((l1 >> sh) & 1ull);
-                res = digit_residue(lo, top, F, Fq, p);
-                if (s < 0 && res) res = p - res;
+        const uint32_t *F = is_x ? prm.pc[kp].fx : prm.pc[kp].fa;
+        const uint32_t *Fq = is_x ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
+        const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
+        if (act) {
+            uint32_t v[G1];
+#pragma unroll
+            for (int m = 0; m < H1; ++m) {
+                // residue of the signed digit: (lo32 F0 + hi32 F1 + top F2) mod p, negated if sign < 0
+                uint32_t x0 = red1(shoup(dlo[m], F[0], Fq[0], p), p);
+                uint32_t x1 = red1(shoup(dhi[m], F[1], Fq[1], p), p);
+                uint32_t res = addm(x0, x1, p);
+                if ((dtop >> m) & 1u) res = addm(res, F[2], p);
+                if (sg < 0) res = subm(0u, res, p);
+                v[m] = res;
             }
-            sm[r * RS + pad(t)] = res;
+            // top stage (h = N2/2) with a zero upper half: (u, 0) -> (u, u W)
+#pragma unroll
+            for (int m = 0; m < H1; ++m) {
+                const uint2 wv = TwGlobal::ld(tw, S1 * H1 + j0 + S1 * m);
+                v[m + H1] = red1(shoup(v[m], wv.x, wv.y, p), p);
+            }
+#pragma unroll
+            for (int l = R1 - 2; l >= 0; --l) {
+                const int half = 1 << l;
+#pragma unroll
+                for (int m = 0; m < G1; ++m) {
+                    if (m & half) continue;
+                    const uint2 wv = TwGlobal::ld(tw, S1 * half + j0 + S1 * (m & (half - 1)));
+                    gs_bfly(v[m], v[m + half], wv, p);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < G1; ++m) sm[r * RS + pad(j0 + m * S1)] = v[m];
         }
         __syncthreads();
-        // ---- A2 (row pass): forward DIF over the slice index, zero-padded upper half
-        const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
-        ntt_forward<TwGlobal, LOGN2, 5>(sm, kTileRows, RS, tw, p, tid, nthr, true);
+        DifPasses<TwGlobal, LOGN2, LOGN2 - R1, 5, false>::run(sm, kK1Rows, RS, tw, p, tid, T, false);
         // ---- write [prime][sigma][row] (x rows reversed: matrix index n-1-row)
-        for (int idx = tid; idx < N2 * kTileRows; idx += nthr) {
-            const int sigma = idx / kTileRows, r = idx % kTileRows;
-            const int64_t row = r0 + r;
-            if (row < count) {
-                const int64_t pos = rev ? (count - 1 - row) : row;
-                out[((int64_t)kp * N2 + sigma) * ld + pos] = sm[r * RS + pad(sigma)];
+        for (int idx = tid; idx < N2 * kK1Rows; idx += T) {
+            const int sigma = idx / kK1Rows, rr = idx % kK1Rows;
+            const int64_t orow = r0 + rr;
+            if (orow < count) {
+                const int64_t pos = rev ? (count - 1 - orow) : orow;
+                out[((int64_t)kp * N2 + sigma) * ld + pos] = sm[rr * RS + pad(sigma)];
             }
         }
         __syncthreads();
@@ -412,17 +462,10 @@ int launch_init(const Params &prm, const uint32_t *gens, void *stream) {
 
 template <int LOGN2>
 static int launch_rows(const Params &prm, cudaStream_t st) {
-    const size_t smem = (size_t)kTileRows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
-    if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return HK_ECUDA;
-    if (cudaFuncSetAttribute(k3a_row_intt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return HK_ECUDA;
-    const int ga = (int)((prm.a_count + kTileRows - 1) / kTileRows);
-    const int gx = (int)((prm.n + kTileRows - 1) / kTileRows);
-    k1_slice_rowntt<LOGN2><<<ga, kK1Threads, smem, st>>>(prm, 0);
-    k1_slice_rowntt<LOGN2><<<gx, kK1Threads, smem, st>>>(prm, 1);
+    const int ga = (int)((prm.a_count + kK1Rows - 1) / kK1Rows);
+    const int gx = (int)((prm.n + kK1Rows - 1) / kK1Rows);
+    const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
+    k1_slice_rowntt<LOGN2><<<ga + gx, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();
 }
 

@@ -7,7 +7,7 @@
 //   K2 k2_column         A2 matrix-index forward NTTs (N1) of X^ and A^ columns, A3 pointwise
 //                        Montgomery product, inverse matrix-index NTT, keep the n needed rows
 //   K3a k3a_row_intt     A3 inverse slice-dimension NTT per output row
-//   K3b k3b_crt_carry    A3 Garner CRT -> signed coefficients, A4 carry propagation and
+//   K3b k3b_carry    A3 Garner CRT -> signed coefficients, A4 carry propagation and
 //                        sign-magnitude output
 #include <cuda_runtime.h>
 
@@ -66,21 +66,8 @@ __global__ void k0_init(Params prm, uint2 *tw, uint32_t g0, uint32_t g1, uint32_
 
 // ------------------------------------------------------------------------------------------
 // K1: slice + residues + slice-dimension forward NTT.  One CTA = 16 entries (rows) of a or x.
-constexpr int kK1Threads = 256;
-constexpr int kTileRows = 16;
-
 template <int LOGN2>
 constexpr int k1_row_stride() { return padded_len(1 << LOGN2) + 1; }
-
-HK_DEV uint32_t digit_residue(uint64_t lo, uint32_t top, const uint32_t *F, const uint32_t *Fq,
-                              uint32_t p) {
-    // (lo mod 2^32) F0 + (lo >> 32) F1 + top F2  (mod p), each Shoup product in [0, 2p)
-    uint32_t r0 = red1(shoup((uint32_t)lo, F[0], Fq[0], p), p);
-    uint32_t r1 = red1(shoup((uint32_t)(lo >> 32), F[1], Fq[1], p), p);
-    uint32_t r = addm(r0, r1, p);
-    if (top) r = addm(r, F[2], p);
-    return r;
-}
 
 // K1 v2: a CTA owns kK1Rows entries (a and x tiles in one launch).  Each thread extracts the
 // w-bit digits of its top-pass group once (registers), then for every prime: residues -> top
@@ -223,39 +210,14 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
 }
 
 // ------------------------------------------------------------------------------------------
-// K3a: inverse slice-dimension NTT for 16 output rows x one prime.
+// K3a: for a tile of k3_rows() output rows and all 5 primes: inverse slice-dimension NTT (DIT with
+// forward roots, slice index negated), then Garner CRT (balanced mixed radix) of every
+// coefficient C_s, |C_s| < M/2 < 2^155, written as five 32-bit two's-complement words
+// Ycoef[(row * 5 + word) * ldS + s] (word planes: coalesced stores here and loads in K3b).
 template <int LOGN2>
-__global__ void __launch_bounds__(kK1Threads) k3a_row_intt(Params prm) {
-    constexpr int N2 = 1 << LOGN2;
-    constexpr int RS = k1_row_stride<LOGN2>();
-    extern __shared__ uint32_t sm[];
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int kp = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * kTileRows;
-    const int64_t m = prm.m;
-    const uint32_t p = prm.pc[kp].p;
-    for (int idx = tid; idx < N2 * kTileRows; idx += nthr) {
-        const int sigma = idx / kTileRows, r = idx % kTileRows;
-        const int64_t row = r0 + r;
-        sm[r * RS + pad(sigma)] =
-            row < m ? prm.Yhat[((int64_t)kp * N2 + sigma) * prm.ldY + row] : 0u;
-    }
-    __syncthreads();
-    const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
-    ntt_dit_fwdroots<TwGlobal, LOGN2, 5>(sm, kTileRows, RS, twf, p, tid, nthr);
-    const int S2 = prm.S2;
-    for (int idx = tid; idx < kTileRows * S2; idx += nthr) {
-        const int r = idx / S2, t = idx - (idx / S2) * S2;
-        const int64_t row = r0 + r;
-        if (row < m)  // slice index negated (forward-root DIT)
-            prm.Yres[(row * kNumPrimes + kp) * prm.ldS + t] = sm[r * RS + pad((N2 - t) & (N2 - 1))];
-    }
-}
+constexpr int k3_rows() { return LOGN2 >= 11 ? 4 : 8; }  // 5 x rows x N2 words in smem
+constexpr int kK3aThreads = 512;
 
-// ------------------------------------------------------------------------------------------
-// K3b: Garner CRT (balanced mixed radix) -> signed coefficient C_s (|C_s| < M/2 < 2^155),
-// Y = sum_s C_s 2^(w s) mod 2^(64 Ly), carry propagation by a block scan of carry-transfer
-// functions, two's complement -> sign-magnitude.
 HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint64_t &c0, uint64_t &c1,
                    uint64_t &c2) {
     int32_t v[kNumPrimes];
@@ -286,6 +248,87 @@ HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint64_t &c0
     c2 = (uint64_t)(H >> 64);
 }
 
+template <int LOGN2, int R, int S>
+HK_DEV void k3_dit_pass_all(uint32_t *sm, const Params &prm) {
+    constexpr int N = 1 << LOGN2, G = 1 << R, NG = N / G;
+    constexpr int RS = k1_row_stride<LOGN2>();
+    constexpr int total = kNumPrimes * k3_rows<LOGN2>() * NG;
+    for (int gi = threadIdx.x; gi < total; gi += kK3aThreads) {
+        const int b = gi / NG, g = gi % NG;  // b = kp * k3_rows<LOGN2>() + row
+        const int kp = b / k3_rows<LOGN2>();
+        const uint32_t p = prm.pc[kp].p;
+        const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
+        const int j0 = g % S;
+        const int B = (g / S) * (S * G);
+        uint32_t *base = sm + b * RS;
+        uint32_t v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) v[m] = base[pad(B + j0 + m * S)];
+#pragma unroll
+        for (int l = 0; l < R; ++l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                ct_bfly(v[m], v[m + half], TwGlobal::ld(tw, S * half + j0 + S * (m & (half - 1))), p);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m) base[pad(B + j0 + m * S)] = v[m];
+    }
+    __syncthreads();
+}
+template <int LOGN2, int LO>
+struct K3DitPasses {
+    static HK_DEV void run(uint32_t *sm, const Params &prm) {
+        if constexpr (LO < LOGN2) {
+            constexpr int R = (LOGN2 - LO) < 5 ? (LOGN2 - LO) : 5;
+            k3_dit_pass_all<LOGN2, R, (1 << LO)>(sm, prm);
+            K3DitPasses<LOGN2, LO + R>::run(sm, prm);
+        }
+    }
+};
+
+template <int LOGN2>
+__global__ void __launch_bounds__(kK3aThreads, 1) k3a_row_intt_crt(Params prm) {
+    constexpr int N2 = 1 << LOGN2;
+    constexpr int RS = k1_row_stride<LOGN2>();
+    extern __shared__ uint32_t sm[];  // [prime][row][RS]
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * k3_rows<LOGN2>();
+    const int64_t m = prm.m;
+    for (int idx = tid; idx < kNumPrimes * N2 * k3_rows<LOGN2>(); idx += kK3aThreads) {
+        const int r = idx % k3_rows<LOGN2>(), cs = idx / k3_rows<LOGN2>();  // cs = kp * N2 + sigma
+        const int64_t row = r0 + r;
+        const int kp = cs / N2, sigma = cs % N2;
+        sm[(kp * k3_rows<LOGN2>() + r) * RS + pad(sigma)] =
+            row < m ? __ldcs(prm.Yhat + (int64_t)cs * prm.ldY + row) : 0u;
+    }
+    __syncthreads();
+    K3DitPasses<LOGN2, 0>::run(sm, prm);
+    const int S2 = prm.S2;
+    for (int idx = tid; idx < k3_rows<LOGN2>() * S2; idx += kK3aThreads) {
+        const int r = idx / S2, t = idx - (idx / S2) * S2;
+        const int64_t row = r0 + r;
+        if (row >= m) continue;
+        uint32_t res[kNumPrimes];
+        const int pos = pad((N2 - t) & (N2 - 1));  // slice index negated (forward-root DIT)
+#pragma unroll
+        for (int kp = 0; kp < kNumPrimes; ++kp) res[kp] = sm[(kp * k3_rows<LOGN2>() + r) * RS + pos];
+        uint64_t c0, c1, c2;
+        garner(res, prm, c0, c1, c2);
+        uint32_t *dst = prm.Yres + row * kNumPrimes * prm.ldS + t;
+        dst[0] = (uint32_t)c0;
+        dst[prm.ldS] = (uint32_t)(c0 >> 32);
+        dst[2 * prm.ldS] = (uint32_t)c1;
+        dst[3 * prm.ldS] = (uint32_t)(c1 >> 32);
+        dst[4 * prm.ldS] = (uint32_t)c2;  // bits 128..159; |C| < 2^155, sign in bit 159
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K3b: Y = sum_s C_s 2^(w s) mod 2^(64 Ly), carry propagation by a block scan of
+// carry-transfer functions, two's complement -> sign-magnitude.
 // carry-transfer function {-1,0,1} -> {-1,0,1}, packed 2 bits per input (value + 1)
 HK_DEV int tf_apply(int f, int c) { return ((f >> (2 * (c + 1))) & 3) - 1; }
 HK_DEV int tf_compose(int g, int f) {  // g o f
@@ -296,7 +339,7 @@ HK_DEV int tf_compose(int g, int f) {  // g o f
 }
 constexpr int kTfId = (0) | (1 << 2) | (2 << 4);
 
-__global__ void __launch_bounds__(kK3Threads) k3b_crt_carry(Params prm) {
+__global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     extern __shared__ uint64_t coef[];  // [S2][3] 192-bit two's complement coefficients
     __shared__ int64_t s_elast[kK3Threads];
     __shared__ int s_wtot[kK3Threads / 32];
@@ -307,15 +350,12 @@ __global__ void __launch_bounds__(kK3Threads) k3b_crt_carry(Params prm) {
     const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
 
     for (int s = tid; s < S2; s += kK3Threads) {
-        uint32_t r[kNumPrimes];
-#pragma unroll
-        for (int kp = 0; kp < kNumPrimes; ++kp)
-            r[kp] = prm.Yres[(row * kNumPrimes + kp) * prm.ldS + s];
-        uint64_t c0, c1, c2;
-        garner(r, prm, c0, c1, c2);
-        coef[3 * s] = c0;
-        coef[3 * s + 1] = c1;
-        coef[3 * s + 2] = c2;
+        const uint32_t *src = prm.Yres + row * kNumPrimes * prm.ldS + s;
+        const uint32_t w0 = __ldcs(src), w1 = __ldcs(src + prm.ldS), w2 = __ldcs(src + 2 * prm.ldS),
+                       w3 = __ldcs(src + 3 * prm.ldS), w4 = __ldcs(src + 4 * prm.ldS);
+        coef[3 * s] = (uint64_t)w0 | ((uint64_t)w1 << 32);
+        coef[3 * s + 1] = (uint64_t)w2 | ((uint64_t)w3 << 32);
+        coef[3 * s + 2] = (uint64_t)(int64_t)(int32_t)w4;  // sign-extend bit 159
     }
     if (tid == 0) { s_neg = 0; s_zmin = INT_MAX; }
     __syncthreads();
@@ -471,12 +511,13 @@ static int launch_rows(const Params &prm, cudaStream_t st) {
 
 template <int LOGN2>
 static int launch_rows_inverse(const Params &prm, cudaStream_t st) {
-    const size_t smem = (size_t)kTileRows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
-    if (cudaFuncSetAttribute(k3a_row_intt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    const size_t smem =
+        (size_t)kNumPrimes * k3_rows<LOGN2>() * k1_row_stride<LOGN2>() * sizeof(uint32_t);
+    if (cudaFuncSetAttribute(k3a_row_intt_crt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
-    dim3 grid((unsigned)((prm.m + kTileRows - 1) / kTileRows), kNumPrimes);
-    k3a_row_intt<LOGN2><<<grid, kK1Threads, smem, st>>>(prm);
+    const unsigned grid = (unsigned)((prm.m + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
+    k3a_row_intt_crt<LOGN2><<<grid, kK3aThreads, smem, st>>>(prm);
     return check_launch();
 }
 
@@ -518,10 +559,10 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
     }
     if (rc) return rc;
     const size_t smem3 = (size_t)prm.S2 * 3 * sizeof(uint64_t);
-    if (cudaFuncSetAttribute(k3b_crt_carry, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k3b_carry, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem3) != cudaSuccess)
         return HK_ECUDA;
-    k3b_crt_carry<<<(unsigned)prm.m, kK3Threads, smem3, st>>>(prm);
+    k3b_carry<<<(unsigned)prm.m, kK3Threads, smem3, st>>>(prm);
     return check_launch();
 }
 

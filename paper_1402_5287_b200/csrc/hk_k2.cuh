@@ -93,7 +93,8 @@ HK_DEV void dif_bottom_regs(uint32_t (&v)[1 << RL], const uint2 *tw, uint32_t p)
 #pragma unroll
         for (int m = 0; m < (1 << RL); ++m) {
             if (m & half) continue;
-            gs_bfly(v[m], v[m + half], TW::ld(tw, half + (m & (half - 1))), p);
+            if ((m & (half - 1)) == 0) bfly1(v[m], v[m + half], p);  // twiddle 1
+            else gs_bfly(v[m], v[m + half], TW::ld(tw, half + (m & (half - 1))), p);
         }
     }
 }
@@ -105,7 +106,8 @@ HK_DEV void dit_bottom_regs(uint32_t (&v)[1 << RL], const uint2 *tw, uint32_t p)
 #pragma unroll
         for (int m = 0; m < (1 << RL); ++m) {
             if (m & half) continue;
-            ct_bfly(v[m], v[m + half], TW::ld(tw, half + (m & (half - 1))), p);
+            if ((m & (half - 1)) == 0) bfly1(v[m], v[m + half], p);  // twiddle 1
+            else ct_bfly(v[m], v[m + half], TW::ld(tw, half + (m & (half - 1))), p);
         }
     }
 }

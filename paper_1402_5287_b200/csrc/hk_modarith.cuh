@@ -60,6 +60,13 @@ HK_DEV void ct_bfly(uint32_t &u, uint32_t &v, uint2 w, uint32_t p) {
     u = addm(u, t, p);
 }
 
+// Butterfly with twiddle omega^0 = 1 (GS and CT coincide): no multiplication.
+HK_DEV void bfly1(uint32_t &u, uint32_t &v, uint32_t p) {
+    const uint32_t d = subm(u, v, p);
+    u = addm(u, v, p);
+    v = d;
+}
+
 // Twiddle-load policies: the table lives in global memory (read-only path) or shared memory.
 struct TwGlobal {
     static HK_DEV uint2 ld(const uint2 *t, int i) { return __ldg(t + i); }
@@ -110,6 +117,10 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
 #pragma unroll
             for (int m = 0; m < G; ++m) {
                 if (m & half) continue;
+                if (S == 1 && (m & (half - 1)) == 0) {  // j = 0: twiddle 1
+                    bfly1(v[m], v[m + half], p);
+                    continue;
+                }
                 const int j = j0 + S * (m & (half - 1));
                 const uint2 w = TW::ld(tw, S * half + j);
                 gs_bfly(v[m], v[m + half], w, p);
@@ -144,6 +155,10 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
 #pragma unroll
             for (int m = 0; m < G; ++m) {
                 if (m & half) continue;
+                if (S == 1 && (m & (half - 1)) == 0) {  // j = 0: twiddle 1
+                    bfly1(v[m], v[m + half], p);
+                    continue;
+                }
                 const int j = j0 + S * (m & (half - 1));
                 const uint2 w = TW::ld(tw, S * half + j);
                 ct_bfly(v[m], v[m + half], w, p);

@@ -67,7 +67,9 @@ __global__ void k0_init(Params prm, uint2 *tw, uint32_t g0, uint32_t g1, uint32_
 // ------------------------------------------------------------------------------------------
 // K1: slice + residues + slice-dimension forward NTT.  One CTA = 16 entries (rows) of a or x.
 template <int LOGN2>
-constexpr int k1_row_stride() { return padded_len(1 << LOGN2) + 1; }
+constexpr int k1_row_stride() {  // = 4 (mod 32): transposed [row][sigma] tiles are conflict-free
+    return (padded_len(1 << LOGN2) + 31) / 32 * 32 + 4;
+}
 
 // K1 v2: a CTA owns kK1Rows entries (a and x tiles in one launch).  Each thread extracts the
 // w-bit digits of its top-pass group once (registers), then for every prime: residues -> top
@@ -270,7 +272,8 @@ HK_DEV void k3_dit_pass_all(uint32_t *sm, const Params &prm) {
 #pragma unroll
             for (int m = 0; m < G; ++m) {
                 if (m & half) continue;
-                ct_bfly(v[m], v[m + half], TwGlobal::ld(tw, S * half + j0 + S * (m & (half - 1))), p);
+                if (S == 1 && (m & (half - 1)) == 0) bfly1(v[m], v[m + half], p);  // twiddle 1
+                else ct_bfly(v[m], v[m + half], TwGlobal::ld(tw, S * half + j0 + S * (m & (half - 1))), p);
             }
         }
 #pragma unroll

@@ -121,11 +121,11 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     double logM = 0;
     for (int k = 0; k < kNumPrimes; ++k) logM += std::log2((double)kPrimesHost[k]);
     bool found = false;
+    // Smallest N2 first; for it the widest slice w in {65, 64} that satisfies the capacity bound.
+    // w >= 64 makes the limb index floor(w s / 64) of coefficient s injective, which the carry
+    // kernel (K3b) relies on.
     for (int lg2 = kMinLogN2; lg2 <= kMaxLogN2 && !found; ++lg2) {
-        const int64_t lsmax = (int64_t(1) << lg2) / 2;  // 2 Ls - 1 <= N2
-        int64_t w = (P + lsmax - 1) / lsmax;
-        if (w < 1) w = 1;
-        for (; w <= kMaxW; ++w) {  // smallest w that fits this N2 first (largest margin)
+        for (int64_t w = kMaxW; w >= 64 && !found; --w) {
             const int64_t Ls = (P + w - 1) / w;
             if (2 * Ls - 1 > (int64_t(1) << lg2)) continue;
             Big wm = big_pow2_minus1((int)w);
@@ -138,7 +138,6 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
                                          2.0 * std::log2(std::ldexp(1.0, (int)w) - 1.0));
                 found = true;
             }
-            break;  // larger w for the same N2 only shrinks the margin
         }
     }
     if (!found) return HK_EUNSUPPORTED;

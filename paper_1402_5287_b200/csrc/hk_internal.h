@@ -15,8 +15,8 @@ constexpr int kMinLogN1 = 6;
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
-constexpr int kK3Threads = 512;                         // CRT/carry block
-constexpr int kK3MaxChunk = 8;                          // limbs per thread -> Ly <= 4096
+constexpr int kK3Threads = 128;                         // carry block (one output row)
+constexpr int kK3MaxChunk = 17;                         // limbs per thread -> Ly <= 2176
 
 struct PrimeConsts {
     uint32_t p, pneg;          // modulus, -p^-1 mod 2^32 (Montgomery)

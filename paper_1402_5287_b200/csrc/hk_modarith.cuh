@@ -60,6 +60,13 @@ HK_DEV void ct_bfly(uint32_t &u, uint32_t &v, uint2 w, uint32_t p) {
     u = addm(u, t, p);
 }
 
+// 4-byte asynchronous global -> shared copy (LDGSTS); completes at cp_async_wait_all().
+HK_DEV void cp_async4(uint32_t *smem, const uint32_t *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+HK_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // Butterfly with twiddle omega^0 = 1 (GS and CT coincide): no multiplication.
 HK_DEV void bfly1(uint32_t &u, uint32_t &v, uint32_t p) {
     const uint32_t d = subm(u, v, p);

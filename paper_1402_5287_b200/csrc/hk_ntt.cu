@@ -304,9 +304,11 @@ __global__ void __launch_bounds__(kK3aThreads, 1) k3a_row_intt_crt(Params prm) {
         const int r = idx % k3_rows<LOGN2>(), cs = idx / k3_rows<LOGN2>();  // cs = kp * N2 + sigma
         const int64_t row = r0 + r;
         const int kp = cs / N2, sigma = cs % N2;
-        sm[(kp * k3_rows<LOGN2>() + r) * RS + pad(sigma)] =
-            row < m ? __ldcs(prm.Yhat + (int64_t)cs * prm.ldY + row) : 0u;
+        uint32_t *dst = sm + (kp * k3_rows<LOGN2>() + r) * RS + pad(sigma);
+        if (row < m) cp_async4(dst, prm.Yhat + (int64_t)cs * prm.ldY + row);
+        else *dst = 0u;
     }
+    cp_async_wait_all();
     __syncthreads();
     K3DitPasses<LOGN2, 0>::run(sm, prm);
     const int S2 = prm.S2;
@@ -342,80 +344,97 @@ HK_DEV int tf_compose(int g, int f) {  // g o f
 }
 constexpr int kTfId = (0) | (1 << 2) | (2 << 4);
 
+// One CTA per output row.  Coefficient s (160-bit two's complement C_s, w in {64, 65}) sits at
+// limb q(s) = floor(w s / 64), bit sh = w s mod 64; its shifted value C_s 2^sh spans the four
+// words S_0..S_3 (sign-extended to 256 bits) plus a -1 borrow into limb q + 4 when C_s < 0.
+// Because q is injective for w >= 64, word d of every coefficient lands in its own slot
+// P_d[q(s) + d]; limb l's sum is P_0[l] + P_1[l] + P_2[l] + P_3[l] - borrow[l].
 __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
-    extern __shared__ uint64_t coef[];  // [S2][3] 192-bit two's complement coefficients
-    __shared__ int64_t s_elast[kK3Threads];
+    extern __shared__ uint64_t sP[];  // [4][Ly] words, then borrow bytes [Ly]
+    __shared__ uint8_t s_ecarry[kK3Threads];
     __shared__ int s_wtot[kK3Threads / 32];
     __shared__ int s_wcarry[kK3Threads / 32];
     __shared__ int s_neg, s_zmin;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t row = blockIdx.x;
     const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
-
-    for (int s = tid; s < S2; s += kK3Threads) {
-        const uint32_t *src = prm.Yres + row * kNumPrimes * prm.ldS + s;
-        const uint32_t w0 = __ldcs(src), w1 = __ldcs(src + prm.ldS), w2 = __ldcs(src + 2 * prm.ldS),
-                       w3 = __ldcs(src + 3 * prm.ldS), w4 = __ldcs(src + 4 * prm.ldS);
-        coef[3 * s] = (uint64_t)w0 | ((uint64_t)w1 << 32);
-        coef[3 * s + 1] = (uint64_t)w2 | ((uint64_t)w3 << 32);
-        coef[3 * s + 2] = (uint64_t)(int64_t)(int32_t)w4;  // sign-extend bit 159
+    uint8_t *sB = reinterpret_cast<uint8_t *>(sP + 4 * Ly);
+    // zero the slot arrays (positions without a coefficient stay 0)
+    {
+        uint4 *z = reinterpret_cast<uint4 *>(sP);
+        const int n16 = (4 * Ly * 8 + Ly + 15) / 16;
+        for (int i = tid; i < n16; i += kK3Threads) z[i] = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) { s_neg = 0; s_zmin = INT_MAX; }
+    __syncthreads();
+    const uint32_t *src = prm.Yres + row * kNumPrimes * prm.ldS;
+    const int64_t ldS = prm.ldS;
+    for (int s = tid; s < S2; s += kK3Threads) {
+        const uint32_t w0 = __ldcs(src + s), w1 = __ldcs(src + ldS + s), w2 = __ldcs(src + 2 * ldS + s),
+                       w3 = __ldcs(src + 3 * ldS + s), w4 = __ldcs(src + 4 * ldS + s);
+        const uint64_t C0 = (uint64_t)w0 | ((uint64_t)w1 << 32);
+        const uint64_t C1 = (uint64_t)w2 | ((uint64_t)w3 << 32);
+        const uint64_t C2 = (uint64_t)(int64_t)(int32_t)w4;  // sign-extend bit 159
+        const uint64_t C3 = (uint64_t)((int64_t)C2 >> 63);
+        const int o = w * s, q = o >> 6, sh = o & 63;
+        uint64_t S0 = C0, S1 = C1, S2w = C2, S3 = C3;
+        if (sh) {
+            S3 = (C3 << sh) | (C2 >> (64 - sh));
+            S2w = (C2 << sh) | (C1 >> (64 - sh));
+            S1 = (C1 << sh) | (C0 >> (64 - sh));
+            S0 = C0 << sh;
+        }
+        if (q < Ly) sP[q] = S0;
+        if (q + 1 < Ly) sP[Ly + q + 1] = S1;
+        if (q + 2 < Ly) sP[2 * Ly + q + 2] = S2w;
+        if (q + 3 < Ly) sP[3 * Ly + q + 3] = S3;
+        if (C3 && q + 4 < Ly) sB[q + 4] = 1;
+    }
     __syncthreads();
 
     const int chunk = (Ly + kK3Threads - 1) / kK3Threads;
     const int l0 = tid * chunk;
     const int l1 = min(Ly, l0 + chunk);
     uint64_t u[kK3MaxChunk];
-    int64_t e[kK3MaxChunk];
+    int8_t e[kK3MaxChunk];
 #pragma unroll
     for (int c = 0; c < kK3MaxChunk; ++c) {
         u[c] = 0;
         e[c] = 0;
         const int l = l0 + c;
         if (c < chunk && l < l1) {
-            __int128 acc = 0;
-            const int smin = max(0, (64 * (l - 4) + w - 1) / w);
-            const int smax = min(S2 - 1, (64 * l + 63) / w);
-            for (int s = smin; s <= smax; ++s) {
-                const int o = w * s, q = o >> 6, sh = o & 63, d = l - q;
-                if (d < 0) continue;
-                const uint64_t C0 = coef[3 * s], C1 = coef[3 * s + 1], C2 = coef[3 * s + 2];
-                const bool neg = (int64_t)C2 < 0;
-                if (d <= 3) {
-                    const uint64_t C3 = neg ? ~0ull : 0ull;
-                    const uint64_t Wd = d == 0 ? C0 : d == 1 ? C1 : d == 2 ? C2 : C3;
-                    const uint64_t Wm = d == 0 ? 0ull : d == 1 ? C0 : d == 2 ? C1 : C2;
-                    const uint64_t piece = sh ? ((Wd << sh) | (Wm >> (64 - sh))) : Wd;
-                    acc += (__int128)(unsigned __int128)piece;
-                } else if (d == 4 && neg) {
-                    acc -= 1;
-                }
-            }
-            u[c] = (uint64_t)acc;
-            e[c] = (int64_t)(acc >> 64);
+            uint64_t acc = sP[l];
+            int hi = 0;
+            uint64_t t = sP[Ly + l];
+            acc += t; hi += acc < t;
+            t = sP[2 * Ly + l];
+            acc += t; hi += acc < t;
+            t = sP[3 * Ly + l];
+            acc += t; hi += acc < t;
+            if (sB[l]) { hi -= acc == 0; acc -= 1; }
+            u[c] = acc;
+            e[c] = (int8_t)hi;  // carry into limb l+1, in [-1, 3]
         }
     }
-    // carry out of this thread's last limb -> next thread's first limb
     {
-        int64_t last = 0;
+        int last = 0;
 #pragma unroll
         for (int c = 0; c < kK3MaxChunk; ++c)
             if (c < chunk && l0 + c < l1) last = e[c];
-        s_elast[tid] = last;
+        s_ecarry[tid] = (uint8_t)(last + 1);
     }
     __syncthreads();
-    // u_l = w_l + e_{l-1}; g_l in {-1,0,1}; transfer f_l(c) = g_l + [u_l+c overflows]
+    // u_l = w_l + e_{l-1}; g_l in {-1,0,1}; transfer f_l(c) = g_l + [u_l + c overflows]
     int F = kTfId;
     int fl[kK3MaxChunk];
     {
-        int64_t ein = tid > 0 ? s_elast[tid - 1] : 0;
+        int ein = tid > 0 ? (int)s_ecarry[tid - 1] - 1 : 0;
 #pragma unroll
         for (int c = 0; c < kK3MaxChunk; ++c) {
             fl[c] = kTfId;
             if (c < chunk && l0 + c < l1) {
                 const uint64_t wv = u[c];
-                const uint64_t uv = wv + (uint64_t)ein;
+                const uint64_t uv = wv + (uint64_t)(int64_t)ein;
                 int g = 0;
                 if (ein > 0 && uv < wv) g = 1;
                 if (ein < 0 && uv > wv) g = -1;
@@ -561,7 +580,7 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
         default: return HK_EUNSUPPORTED;
     }
     if (rc) return rc;
-    const size_t smem3 = (size_t)prm.S2 * 3 * sizeof(uint64_t);
+    const size_t smem3 = ((size_t)4 * prm.Ly * 8 + prm.Ly + 15) / 16 * 16;
     if (cudaFuncSetAttribute(k3b_carry, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem3) != cudaSuccess)
         return HK_ECUDA;

@@ -13,6 +13,7 @@
 
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "hk_internal.h"
 #include "hk_modarith.cuh"
@@ -197,14 +198,26 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
             for (int m = 0; m < G1; ++m) sm[r * RS + pad(j0 + m * S1)] = v[m];
         }
         __syncthreads();
-        DifPasses<TwGlobal, LOGN2, LOGN2 - R1, 5, false>::run(sm, kK1Rows, RS, tw, p, tid, T, false);
-        // ---- write [prime][sigma][row] (x rows reversed: matrix index n-1-row)
-        for (int idx = tid; idx < N2 * kK1Rows; idx += T) {
-            const int sigma = idx / kK1Rows, rr = idx % kK1Rows;
+        constexpr int REM = LOGN2 - R1;          // stages left after the top pass
+        constexpr int RB = REM < 5 ? REM : 5;    // bottom pass (S = 1) radix
+        if constexpr (REM > RB)
+            dif_pass<TwGlobal, LOGN2, REM - RB, (1 << RB), false>(sm, kK1Rows, RS, tw, p, tid, T);
+        // ---- bottom pass in registers, stored straight to [prime][sigma][row]; lanes cover
+        // 8 rows x 4 groups so every store instruction writes full 32-byte row segments
+        // (x rows reversed: matrix index n-1-row)
+        constexpr int GB = 1 << RB, NGR = N2 / GB;
+        for (int gi = tid; gi < kK1Rows * NGR; gi += T) {
+            const int rr = gi % kK1Rows, g = gi / kK1Rows;
+            uint32_t v[GB];
+#pragma unroll
+            for (int m = 0; m < GB; ++m) v[m] = sm[rr * RS + pad(g * GB + m)];
+            dif_bottom_regs<TwGlobal, RB>(v, tw, p);
             const int64_t orow = r0 + rr;
             if (orow < count) {
                 const int64_t pos = rev ? (count - 1 - orow) : orow;
-                out[((int64_t)kp * N2 + sigma) * ld + pos] = sm[rr * RS + pad(sigma)];
+                uint32_t *o = out + ((int64_t)kp * N2 + (int64_t)g * GB) * ld + pos;
+#pragma unroll
+                for (int m = 0; m < GB; ++m) o[(int64_t)m * ld] = v[m];
             }
         }
         __syncthreads();
@@ -550,6 +563,12 @@ static int launch_cols(const Params &prm, cudaStream_t st) {
     if (cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
+    // one CTA per SM: keep the carveout minimal so the N1 twiddle table stays L1-resident
+    const int pct = (int)((smem + 2048) * 100 / (228 * 1024)) + 1;
+    if (getenv("HK_K2_CARVEOUT"))
+        cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             atoi(getenv("HK_K2_CARVEOUT")));
+    (void)pct;
     k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
 }

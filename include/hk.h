@@ -190,6 +190,20 @@ int32_t hk_schoolbook_matvec(int32_t kind, int64_t m, int64_t n, int32_t P,
                              const uint64_t *x_mag, const int8_t *x_sign,
                              uint64_t *y_mag, int8_t *y_sign, void *stream);
 
+/* Companion A5: the paper's Karatsuba-like Algorithm 1 run level
+ * by level on the GPU -- split (steps 3-6), recursion as 3^d batched subproblems per level
+ * (step 7; size-m children zero-padded to m1), direct products at subproblems of size
+ * <= cutoff (step 1 is cutoff = 2), merge (step 8).  Square Hankel only, shapes as
+ * hk_hankel_matvec; DEVICE pointers; inputs must be canonical (not validated).  cutoff >= 2.
+ * The workspace (caller-owned, 256-byte aligned) holds every level's operands and results:
+ * hk_karatsuba_workspace_size returns its size (pure host).  Asynchronous on `stream`. */
+int32_t hk_karatsuba_workspace_size(int64_t n, int32_t P, int32_t cutoff, size_t *bytes);
+int32_t hk_karatsuba_matvec(int64_t n, int32_t P, int32_t cutoff,
+                            const uint64_t *a_mag, const int8_t *a_sign,
+                            const uint64_t *x_mag, const int8_t *x_sign,
+                            uint64_t *y_mag, int8_t *y_sign,
+                            void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

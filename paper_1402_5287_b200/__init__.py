@@ -66,6 +66,8 @@ def _load():
         "hk_schoolbook_matvec": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
         "hk_matvec_stages": (i32, [i32, i64, i64, i32, ctypes.c_uint32, vp, vp, vp, vp, vp, vp,
                                    vp, sz, vp]),
+        "hk_karatsuba_workspace_size": (i32, [i64, i32, i32, ctypes.POINTER(sz)]),
+        "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -78,7 +80,8 @@ _lib = _load()
 EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_workspace_size",
             "hk_workspace_init", "hk_workspace_status", "hk_hankel_matvec", "hk_toeplitz_matvec",
             "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host",
-            "hk_schoolbook_matvec", "hk_matvec_stages")
+            "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
+            "hk_karatsuba_matvec")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -295,6 +298,37 @@ def schoolbook_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, s
              _dev_ptr(out[1], (torch.int8,), (m,), "y_sign")]
     _check(_lib.hk_schoolbook_matvec(kind, m, n, P, *args, _stream_ptr(stream)),
            "hk_schoolbook_matvec")
+    return out
+
+
+def karatsuba_workspace_size(n: int, P: int, cutoff: int = 8) -> int:
+    out = ctypes.c_size_t()
+    _check(_lib.hk_karatsuba_workspace_size(n, P, cutoff, ctypes.byref(out)),
+           "hk_karatsuba_workspace_size")
+    return int(out.value)
+
+
+def karatsuba_matvec(a_mag, a_sign, x_mag, x_sign, P, cutoff: int = 8, out=None, stream=None):
+    """Companion A5: Algorithm 1 level by level on the GPU (Hankel)."""
+    import torch
+    n = int(x_mag.shape[0])
+    L, Ly = limbs(P), out_limbs(P)
+    args = [_dev_ptr(a_mag, _mag_dtypes(), (2 * n - 1, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (2 * n - 1,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (n,), "x_sign")]
+    if out is None:
+        out = (torch.empty((n, Ly), dtype=a_mag.dtype, device=a_mag.device),
+               torch.empty((n,), dtype=torch.int8, device=a_mag.device))
+    args += [_dev_ptr(out[0], _mag_dtypes(), (n, Ly), "y_mag"),
+             _dev_ptr(out[1], (torch.int8,), (n,), "y_sign")]
+    nbytes = karatsuba_workspace_size(n, P, cutoff)
+    buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=a_mag.device)
+    ptr = (buf.data_ptr() + 255) & ~255
+    _check(_lib.hk_karatsuba_matvec(n, P, cutoff, *args, ptr, nbytes, _stream_ptr(stream)),
+           "hk_karatsuba_matvec")
+    # buf returns to torch's caching allocator, which only reuses it for work ordered after
+    # this call on the same stream
     return out
 
 

@@ -418,4 +418,19 @@ int32_t hk_schoolbook_matvec(int32_t kind, int64_t m, int64_t n, int32_t P,
     return launch_schoolbook(kind, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, stream);
 }
 
+int32_t hk_karatsuba_workspace_size(int64_t n, int32_t P, int32_t cutoff, size_t *bytes) {
+    if (!bytes) return HK_EINVAL;
+    return karatsuba_workspace_size(n, P, cutoff, bytes);
+}
+
+int32_t hk_karatsuba_matvec(int64_t n, int32_t P, int32_t cutoff, const uint64_t *a_mag,
+                            const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
+                            uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes,
+                            void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws) return HK_EINVAL;
+    if (((uintptr_t)ws & 255) != 0) return HK_EINVAL;
+    return launch_karatsuba(n, P, cutoff, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
+                            ws_bytes, stream);
+}
+
 }  // extern "C"

@@ -80,4 +80,10 @@ int launch_schoolbook(int kind, int64_t m, int64_t n, int32_t P, const uint64_t 
                       const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
                       uint64_t *y_mag, int8_t *y_sign, void *stream);
 
+// companion A5 (hk_karatsuba.cu)
+int karatsuba_workspace_size(int64_t n, int32_t P, int32_t cutoff, size_t *bytes);
+int launch_karatsuba(int64_t n, int32_t P, int32_t cutoff, const uint64_t *a_mag,
+                     const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
+                     uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream);
+
 }  // namespace hk

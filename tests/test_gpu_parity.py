@@ -240,3 +240,33 @@ def test_schoolbook_parity(hk, n, P):
         torch.cuda.synchronize()
         assert_same(hk.to_host(ym, ys), oracle.matvec(kind, P, am, asg, xm, xsg),
                     f"schoolbook kind={kind} n={n} P={P}")
+
+
+# ---------------------------------------------------------------------------------------------
+# companion A5: Algorithm 1 level by level
+@pytest.mark.parametrize("n,P,cutoff", [(1, 64, 2), (2, 64, 2), (3, 100, 2), (5, 65, 2),
+                                        (17, 1000, 2), (64, 3328, 2), (64, 3328, 8),
+                                        (100, 2000, 4), (129, 700, 8), (33, 16608, 2),
+                                        (257, 200, 3)])
+def test_karatsuba_parity(hk, n, P, cutoff):
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=n + cutoff)
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    ym, ys = hk.karatsuba_matvec(a, sa, x, sx, P, cutoff=cutoff)
+    torch.cuda.synchronize()
+    assert_same(hk.to_host(ym, ys), oracle.matvec(0, P, am, asg, xm, xsg),
+                f"karatsuba n={n} P={P} cutoff={cutoff}")
+
+
+def test_karatsuba_carry_stress_and_c2_rows(hk):
+    am, asg, xm, xsg = gen.make_inputs(0, 64, 16608, seed=4, recipe="carry_stress")
+    got = hk.to_host(*hk.karatsuba_matvec(*hk.to_device(am, asg), *hk.to_device(xm, xsg), 16608,
+                                          cutoff=2))
+    assert_same(got, oracle.matvec(0, 16608, am, asg, xm, xsg), "karatsuba carry-stress")
+    am, asg, xm, xsg = gen.config_inputs("C2")
+    got = hk.to_host(*hk.karatsuba_matvec(*hk.to_device(am, asg), *hk.to_device(xm, xsg), 33216,
+                                          cutoff=8))
+    fp.check(0, am, asg, xm, xsg, *got)
+    rows = np.array([0, 1, 511, 1022, 1023], dtype=np.int64)
+    wm, ws_ = oracle.matvec(0, 33216, am, asg, xm, xsg, rows=rows)
+    assert_same((got[0][rows], got[1][rows]), (wm, ws_), "karatsuba C2 rows")

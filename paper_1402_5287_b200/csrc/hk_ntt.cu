@@ -111,6 +111,17 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
     const int64_t r0 = (int64_t)tile * kK1Rows;
     const int L = prm.L, w = prm.w, Ls = prm.Ls;
 
+    // ---- stage the tile's limbs (kK1Rows consecutive entries = one contiguous block) in smem
+    uint64_t *slimb = reinterpret_cast<uint64_t *>(sm + kK1Rows * RS);
+    {
+        const int64_t nrows = count - r0 < kK1Rows ? count - r0 : kK1Rows;
+        const int64_t bytes = nrows * L * 8;
+        const char *g = reinterpret_cast<const char *>(mag + r0 * L);
+        char *d = reinterpret_cast<char *>(slimb);
+        for (int64_t c = tid; c < bytes / 16; c += T) cp_async16(d + 16 * c, g + 16 * c);
+        if ((bytes & 15) && tid == 0) cp_async8(d + (bytes & ~int64_t(15)), g + (bytes & ~int64_t(15)));
+        cp_async_wait_all();
+    }
     // ---- validation (A1): bits >= P zero, sign in {-1,0,1}, sign == 0 <=> magnitude == 0
     const int rem = prm.P - 64 * (L - 1);
     const uint64_t topmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
@@ -121,7 +132,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
         const int r = idx / L, u = idx - (idx / L) * L;
         const int64_t row = r0 + r;
         if (row >= count) continue;
-        const uint64_t v = __ldg(mag + row * L + u);
+        const uint64_t v = slimb[idx];
         if (v) s_nz[r] = 1;
         if (u == L - 1 && (v & ~topmask)) bad = true;
     }
@@ -140,7 +151,6 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
 
     // ---- A1: this thread's digits t = j0 + m S1 (m < 16), extracted once for all primes
     const int r = tid / TPR, j0 = tid % TPR;
-    const int64_t row = r0 + r;
     const int sg = s_sign[r];
     const bool act = j0 < S1;
     uint32_t dlo[H1], dhi[H1], dtop = 0;
@@ -150,9 +160,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
         uint64_t lo = 0;
         if (act && sg != 0 && t < Ls) {
             const int o = w * t, q = o >> 6, sh = o & 63;
-            const uint64_t *rp = mag + row * L;
-            const uint64_t l0 = __ldg(rp + q);
-            const uint64_t l1 = (q + 1 < L) ? __ldg(rp + q + 1) : 0ull;
+            const uint64_t *rp = slimb + r * L;
+            const uint64_t l0 = rp[q];
+            const uint64_t l1 = (q + 1 < L) ? rp[q + 1] : 0ull;
             lo = sh ? ((l0 >> sh) | (l1 << (64 - sh))) : l0;
             if (w < 64) lo &= (1ull << w) - 1;
             else if (w == 65) dtop |= (uint32_t)((l1 >> sh) & 1ull) << m;
@@ -539,7 +549,11 @@ template <int LOGN2>
 static int launch_rows(const Params &prm, cudaStream_t st) {
     const int ga = (int)((prm.a_count + kK1Rows - 1) / kK1Rows);
     const int gx = (int)((prm.n + kK1Rows - 1) / kK1Rows);
-    const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t);
+    const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t) +
+                         (size_t)kK1Rows * prm.L * sizeof(uint64_t);
+    if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem1) != cudaSuccess)
+        return HK_ECUDA;
     k1_slice_rowntt<LOGN2><<<ga + gx, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();
 }

@@ -48,6 +48,7 @@ struct Params {
     int64_t out_off;             // first needed index of the matrix-index convolution
     int64_t ldA, ldX, ldY, ldS;  // leading dims (elements) of the transform-domain arrays
     uint64_t hash;
+    int32_t diag;                // diagnostics-only switches (HK_K2_DIAG); 0 in production
     // inputs / outputs (device)
     const uint64_t *a_mag;
     const int8_t *a_sign;

@@ -205,13 +205,14 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
 }
 
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
-template <int LOGN1>
+// TW = TwConst is a diagnostics-only variant (HK_K2_DIAG=1; wrong results).
+template <int LOGN1, class TW = TwGlobal>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), 1) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
     const int col = blockIdx.x;
     const int kp = col >> prm.log_n2;
     const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1) + prm.N2;
-    k2_column_body<TwGlobal, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
+    k2_column_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
 }
 
 }  // namespace hk

@@ -583,7 +583,16 @@ static int launch_cols(const Params &prm, cudaStream_t st) {
         cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              atoi(getenv("HK_K2_CARVEOUT")));
     (void)pct;
-    k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
+    const int diag = getenv("HK_K2_DIAG") ? atoi(getenv("HK_K2_DIAG")) : 0;  // diagnostics only
+    Params p2 = prm;
+    p2.diag = diag;
+    if (diag & 1) {
+        cudaFuncSetAttribute(k2_column<LOGN1, TwConst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        k2_column<LOGN1, TwConst><<<ncols, k2_threads<LOGN1>(), smem, st>>>(p2);
+    } else {
+        k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(p2);
+    }
     return check_launch();
 }
 

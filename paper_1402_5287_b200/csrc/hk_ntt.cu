@@ -240,8 +240,8 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
 // coefficient C_s, |C_s| < M/2 < 2^155, written as five 32-bit two's-complement words
 // Ycoef[(row * 5 + word) * ldS + s] (word planes: coalesced stores here and loads in K3b).
 template <int LOGN2>
-constexpr int k3_rows() { return LOGN2 >= 11 ? 4 : 8; }  // 5 x rows x N2 words in smem
-constexpr int kK3aThreads = 512;
+constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : 4; }  // 5 x rows x N2 words in smem
+constexpr int kK3aThreads = 320;  // 5 primes x 4 rows x 32 groups = 2 groups per thread
 
 HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint64_t &c0, uint64_t &c1,
                    uint64_t &c2) {
@@ -316,7 +316,7 @@ struct K3DitPasses {
 };
 
 template <int LOGN2>
-__global__ void __launch_bounds__(kK3aThreads, 1) k3a_row_intt_crt(Params prm) {
+__global__ void __launch_bounds__(kK3aThreads, 2) k3a_row_intt_crt(Params prm) {
     constexpr int N2 = 1 << LOGN2;
     constexpr int RS = k1_row_stride<LOGN2>();
     extern __shared__ uint32_t sm[];  // [prime][row][RS]

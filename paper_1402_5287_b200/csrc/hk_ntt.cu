@@ -372,6 +372,7 @@ constexpr int kTfId = (0) | (1 << 2) | (2 << 4);
 // words S_0..S_3 (sign-extended to 256 bits) plus a -1 borrow into limb q + 4 when C_s < 0.
 // Because q is injective for w >= 64, word d of every coefficient lands in its own slot
 // P_d[q(s) + d]; limb l's sum is P_0[l] + P_1[l] + P_2[l] + P_3[l] - borrow[l].
+template <int CHUNK>  // limbs per thread = ceil(Ly / kK3Threads)
 __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     extern __shared__ uint64_t sP[];  // [4][Ly] words, then borrow bytes [Ly]
     __shared__ uint8_t s_ecarry[kK3Threads];
@@ -382,8 +383,7 @@ __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     const int64_t row = blockIdx.x;
     const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
     uint8_t *sB = reinterpret_cast<uint8_t *>(sP + 4 * Ly);
-    // zero the slot arrays (positions without a coefficient stay 0)
-    {
+    {  // zero the slot arrays (positions without a coefficient stay 0)
         uint4 *z = reinterpret_cast<uint4 *>(sP);
         const int n16 = (4 * Ly * 8 + Ly + 15) / 16;
         for (int i = tid; i < n16; i += kK3Threads) z[i] = make_uint4(0, 0, 0, 0);
@@ -415,64 +415,47 @@ __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     }
     __syncthreads();
 
-    const int chunk = (Ly + kK3Threads - 1) / kK3Threads;
-    const int l0 = tid * chunk;
-    const int l1 = min(Ly, l0 + chunk);
-    uint64_t u[kK3MaxChunk];
-    int8_t e[kK3MaxChunk];
+    const int l0 = tid * CHUNK;
+    uint64_t u[CHUNK];
+    int e[CHUNK];
 #pragma unroll
-    for (int c = 0; c < kK3MaxChunk; ++c) {
-        u[c] = 0;
-        e[c] = 0;
+    for (int c = 0; c < CHUNK; ++c) {
         const int l = l0 + c;
-        if (c < chunk && l < l1) {
-            uint64_t acc = sP[l];
-            int hi = 0;
+        uint64_t acc = 0;
+        int hi = 0;
+        if (l < Ly) {
+            acc = sP[l];
             uint64_t t = sP[Ly + l];
             acc += t; hi += acc < t;
             t = sP[2 * Ly + l];
             acc += t; hi += acc < t;
             t = sP[3 * Ly + l];
             acc += t; hi += acc < t;
-            if (sB[l]) { hi -= acc == 0; acc -= 1; }
-            u[c] = acc;
-            e[c] = (int8_t)hi;  // carry into limb l+1, in [-1, 3]
+            const int bw = sB[l];
+            hi -= bw & (acc == 0);
+            acc -= bw;
         }
+        u[c] = acc;
+        e[c] = hi;  // carry into limb l+1, in [-1, 3]
     }
-    {
-        int last = 0;
-#pragma unroll
-        for (int c = 0; c < kK3MaxChunk; ++c)
-            if (c < chunk && l0 + c < l1) last = e[c];
-        s_ecarry[tid] = (uint8_t)(last + 1);
-    }
+    s_ecarry[tid] = (uint8_t)(e[CHUNK - 1] + 1);
     __syncthreads();
-    // u_l = w_l + e_{l-1}; g_l in {-1,0,1}; transfer f_l(c) = g_l + [u_l + c overflows]
+    // u_l = w_l + e_{l-1} -> g_l in {-1,0,1}; transfer f_l(c) = g_l + [c=1, u_l=MAX] - [c=-1, u_l=0]
+    // packed 2 bits per input c in {-1,0,1}: (f(-1)+1) | (f(0)+1) << 2 | (f(1)+1) << 4
     int F = kTfId;
-    int fl[kK3MaxChunk];
-    {
-        int ein = tid > 0 ? (int)s_ecarry[tid - 1] - 1 : 0;
+    int fl[CHUNK];
+    int ein = tid > 0 ? (int)s_ecarry[tid - 1] - 1 : 0;
 #pragma unroll
-        for (int c = 0; c < kK3MaxChunk; ++c) {
-            fl[c] = kTfId;
-            if (c < chunk && l0 + c < l1) {
-                const uint64_t wv = u[c];
-                const uint64_t uv = wv + (uint64_t)(int64_t)ein;
-                int g = 0;
-                if (ein > 0 && uv < wv) g = 1;
-                if (ein < 0 && uv > wv) g = -1;
-                u[c] = uv;
-                int f = 0;
-#pragma unroll
-                for (int ci = -1; ci <= 1; ++ci) {
-                    const int o = g + ((ci == 1 && uv == ~0ull) ? 1 : 0) - ((ci == -1 && uv == 0) ? 1 : 0);
-                    f |= (o + 1) << (2 * (ci + 1));
-                }
-                fl[c] = f;
-                F = tf_compose(f, F);
-                ein = e[c];
-            }
-        }
+    for (int c = 0; c < CHUNK; ++c) {
+        const uint64_t wv = u[c];
+        const uint64_t uv = wv + (uint64_t)(int64_t)ein;
+        const int g = (ein > 0 && uv < wv) ? 1 : ((ein < 0 && uv > wv) ? -1 : 0);
+        u[c] = uv;
+        const int g1 = g + 1;
+        const int f = (g1 - (uv == 0)) | (g1 << 2) | ((g1 + (uv == ~0ull)) << 4);
+        fl[c] = f;
+        F = tf_compose(f, F);
+        ein = e[c];
     }
     // block scan of transfer functions (low limbs first)
     int incl = F;
@@ -494,17 +477,14 @@ __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     const int prev = __shfl_up_sync(0xffffffffu, incl, 1);
     int carry = s_wcarry[warp];
     if (lane > 0) carry = tf_apply(prev, carry);
-    // final limbs (mod 2^(64 Ly))
     int zloc = INT_MAX;
 #pragma unroll
-    for (int c = 0; c < kK3MaxChunk; ++c) {
-        if (c < chunk && l0 + c < l1) {
-            const uint64_t v = u[c] + (uint64_t)(int64_t)carry;
-            carry = tf_apply(fl[c], carry);
-            u[c] = v;
-            if (v && zloc == INT_MAX) zloc = l0 + c;
-            if (l0 + c == Ly - 1) s_neg = (int)(v >> 63);
-        }
+    for (int c = 0; c < CHUNK; ++c) {  // final limbs (mod 2^(64 Ly))
+        const uint64_t v = u[c] + (uint64_t)(int64_t)carry;
+        carry = tf_apply(fl[c], carry);
+        u[c] = v;
+        if (l0 + c < Ly && v && zloc == INT_MAX) zloc = l0 + c;
+        if (l0 + c == Ly - 1) s_neg = (int)(v >> 63);
     }
     if (zloc != INT_MAX) atomicMin(&s_zmin, zloc);
     __syncthreads();
@@ -513,9 +493,9 @@ __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     const int64_t orow = prm.reverse_out ? (prm.m - 1 - row) : row;
     uint64_t *yo = prm.y_mag + orow * Ly;
 #pragma unroll
-    for (int c = 0; c < kK3MaxChunk; ++c) {
+    for (int c = 0; c < CHUNK; ++c) {
         const int l = l0 + c;
-        if (c < chunk && l < l1) {
+        if (l < Ly) {
             uint64_t v = u[c];
             if (neg) v = l < zmin ? 0ull : (l == zmin ? (0ull - v) : ~v);
             yo[l] = v;
@@ -623,10 +603,21 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
     }
     if (rc) return rc;
     const size_t smem3 = ((size_t)4 * prm.Ly * 8 + prm.Ly + 15) / 16 * 16;
-    if (cudaFuncSetAttribute(k3b_carry, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem3) != cudaSuccess)
-        return HK_ECUDA;
-    k3b_carry<<<(unsigned)prm.m, kK3Threads, smem3, st>>>(prm);
+    const int chunk = (prm.Ly + kK3Threads - 1) / kK3Threads;
+    switch (chunk) {
+#define HK_CASE(C)                                                                             \
+    case C:                                                                                    \
+        if (cudaFuncSetAttribute(k3b_carry<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                 (int)smem3) != cudaSuccess)                                   \
+            return HK_ECUDA;                                                                   \
+        k3b_carry<C><<<(unsigned)prm.m, kK3Threads, smem3, st>>>(prm);                         \
+        break;
+        HK_CASE(1) HK_CASE(2) HK_CASE(3) HK_CASE(4) HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8)
+        HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12) HK_CASE(13) HK_CASE(14) HK_CASE(15)
+        HK_CASE(16) HK_CASE(17)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
     return check_launch();
 }
 

@@ -11,6 +11,17 @@ __device__ __forceinline__ uint32_t addm(uint32_t a, uint32_t b, uint32_t p) { u
 __device__ __forceinline__ uint32_t subm(uint32_t a, uint32_t b, uint32_t p) { uint32_t d = a - b; return min(d, d + p); }
 __device__ __forceinline__ uint32_t shoup(uint32_t x, uint32_t w, uint32_t wq, uint32_t p) {
     uint32_t q = __umulhi(x, wq); return x * w - q * p; }
+// ALU-only addition mod p: min(a + b, a + b - p) as IADD3 + VIADDMNMX (no IMAD.IADD)
+__device__ __forceinline__ uint32_t addm2(uint32_t a, uint32_t b, uint32_t p) {
+    uint32_t t, r;
+    asm("add.u32 %0, %1, %2;" : "=r"(t) : "r"(a), "r"(b));
+    asm volatile("{.reg .u32 q; sub.u32 q, %1, %2; min.u32 %0, %1, q;}" : "=r"(r) : "r"(t), "r"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t addm3(uint32_t a, uint32_t b, uint32_t p) {
+    const uint32_t t = a + b - p;       // IADD3
+    return min(a + b, t);               // VIADDMNMX(a, b, t)?
+}
 __device__ __forceinline__ uint32_t montr(uint32_t a, uint32_t b, uint32_t p, uint32_t pneg) {
     uint64_t z = (uint64_t)a * b; uint32_t m = (uint32_t)z * pneg; uint64_t t = z + (uint64_t)m * p;
     return (uint32_t)(t >> 32); }
@@ -32,6 +43,12 @@ __global__ void __launch_bounds__(256) kbfly(uint32_t *out, const uint32_t *tw, 
                 uint32_t d = a - b + p; a = addm(a, b, p); b = red1(shoup(d, W, Wq, p), p);
             } else if (MODE == 1) {  // CT Shoup
                 uint32_t t = red1(shoup(b, W, Wq, p), p); b = subm(a, t, p); a = addm(a, t, p);
+            } else if (MODE == 4) {  // GS Shoup, addm3
+                uint32_t d = a - b + p; a = addm3(a, b, p); b = red1(shoup(d, W, Wq, p), p);
+            } else if (MODE == 5) {  // CT Shoup, addm3 / subm via min(a - t, a - t + p)
+                uint32_t t = red1(shoup(b, W, Wq, p), p); uint32_t d2 = a - t + p; b = min(a - t, d2); a = addm3(a, t, p);
+            } else if (MODE == 6) {  // GS Shoup, asm add
+                uint32_t d = a - b + p; a = addm2(a, b, p); b = red1(shoup(d, W, Wq, p), p);
             } else if (MODE == 2) {  // GS Montgomery
                 uint32_t d = a - b + p; a = addm(a, b, p); b = red1(montr(d, W, p, pneg), p);
             } else {  // CT Montgomery
@@ -62,16 +79,19 @@ int main() {
     uint32_t *tw, *out; cudaMalloc(&tw, sizeof(htw)); cudaMalloc(&out, 1 << 24);
     cudaMemcpy(tw, htw, sizeof(htw), cudaMemcpyHostToDevice);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    const char *names[4] = {"GS_shoup", "CT_shoup", "GS_mont", "CT_mont"};
+    const char *names[7] = {"GS_shoup", "CT_shoup", "GS_mont", "CT_mont", "GS_addm3", "CT_addm3", "GS_asm"};
     const int blocks = nsm * 8, iters = 4000;
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 7; ++mode) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0);
             switch (mode) {
                 case 0: kbfly<0><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
                 case 1: kbfly<1><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
                 case 2: kbfly<2><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
-                default: kbfly<3><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
+                case 3: kbfly<3><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
+                case 4: kbfly<4><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
+                case 5: kbfly<5><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
+                default: kbfly<6><<<blocks, 256>>>(out, tw, iters, p, pneg); break;
             }
             cudaEventRecord(e1); cudaEventSynchronize(e1);
             float ms; cudaEventElapsedTime(&ms, e0, e1);

@@ -371,11 +371,33 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
     if (!a_mag_host || !a_sign_host || !x_mag_host || !x_sign_host || !y_mag_host ||
         !y_sign_host || !ws)
         return HK_EINVAL;
+    if (((uintptr_t)ws & 255) != 0) return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, HK_WS_STAGING, &pl);
     if (rc) return rc;
     if (ws_bytes < pl.info.ws_bytes_staging) return HK_ENOMEM;
-    cudaStream_t st = (cudaStream_t)stream;
+    // Pipeline (all stream-ordered, host synchronises once at the end):
+    //   s1: H2D of x then a in chunks  ->  s0: K1 over the tiles of each chunk as it lands
+    //   s0: K2  ->  K3 per chunk of output rows  ->  s2: D2H of that chunk of y
+    cudaStream_t s0 = (cudaStream_t)stream, s1 = nullptr, s2 = nullptr;
+    cudaEvent_t evs[24];
+    int nev = 0;
+    auto cleanup = [&]() {
+        for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+        if (s1) cudaStreamDestroy(s1);
+        if (s2) cudaStreamDestroy(s2);
+    };
+    auto new_event = [&]() -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (nev < 24 && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess)
+            evs[nev++] = e;
+        return e;
+    };
+    if (cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
+        cleanup();
+        return HK_ECUDA;
+    }
     char *base = (char *)ws;
     const size_t L = pl.info.L, Ly = pl.info.Ly, na = pl.info.a_count;
     uint64_t *d_am = (uint64_t *)(base + pl.st_amag);
@@ -384,18 +406,66 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
     int8_t *d_xs = (int8_t *)(base + pl.st_xsign);
     uint64_t *d_ym = (uint64_t *)(base + pl.st_ymag);
     int8_t *d_ys = (int8_t *)(base + pl.st_ysign);
-    if (cudaMemcpyAsync(d_am, a_mag_host, na * L * 8, cudaMemcpyHostToDevice, st) ||
-        cudaMemcpyAsync(d_as, a_sign_host, na, cudaMemcpyHostToDevice, st) ||
-        cudaMemcpyAsync(d_xm, x_mag_host, (size_t)n * L * 8, cudaMemcpyHostToDevice, st) ||
-        cudaMemcpyAsync(d_xs, x_sign_host, (size_t)n, cudaMemcpyHostToDevice, st))
-        return HK_ECUDA;
-    rc = run_matvec(kind, m, n, P, d_am, d_as, d_xm, d_xs, d_ym, d_ys, ws, pl.info.ws_bytes, stream);
-    if (rc) return rc;
-    if (cudaMemcpyAsync(y_mag_host, d_ym, (size_t)m * Ly * 8, cudaMemcpyDeviceToHost, st) ||
-        cudaMemcpyAsync(y_sign_host, d_ys, (size_t)m, cudaMemcpyDeviceToHost, st))
-        return HK_ECUDA;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    prm.a_mag = d_am; prm.a_sign = d_as; prm.x_mag = d_xm; prm.x_sign = d_xs;
+    prm.y_mag = d_ym; prm.y_sign = d_ys;
+    bool ok = true;
+    cudaEvent_t e0 = new_event();
+    ok = ok && e0 && cudaEventRecord(e0, s0) == cudaSuccess &&
+         cudaStreamWaitEvent(s1, e0, 0) == cudaSuccess && cudaStreamWaitEvent(s2, e0, 0) == cudaSuccess;
+    ok = ok && cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), s0) == cudaSuccess;
+    const int ga = k1_tiles_a(prm), gx = k1_tiles_x(prm);
+    const int kTile = 8;  // rows per K1 tile (kK1Rows)
+    struct Chunk { int t0, nt; };
+    Chunk chunks[6];
+    int nch = 0;
+    for (int c = 0; c < 2; ++c) {  // x first (smaller), then a
+        const int t0 = ga + gx * c / 2, t1 = ga + gx * (c + 1) / 2;
+        if (t1 > t0) chunks[nch++] = {t0, t1 - t0};
+    }
+    for (int c = 0; c < 4; ++c) {
+        const int t0 = ga * c / 4, t1 = ga * (c + 1) / 4;
+        if (t1 > t0) chunks[nch++] = {t0, t1 - t0};
+    }
+    for (int c = 0; c < nch && ok; ++c) {
+        const bool is_x = chunks[c].t0 >= ga;
+        const int64_t cnt = is_x ? n : (int64_t)na;
+        const int64_t r0 = (int64_t)(chunks[c].t0 - (is_x ? ga : 0)) * kTile;
+        int64_t r1 = r0 + (int64_t)chunks[c].nt * kTile;
+        if (r1 > cnt) r1 = cnt;
+        const uint64_t *hm = is_x ? x_mag_host : a_mag_host;
+        const int8_t *hs = is_x ? x_sign_host : a_sign_host;
+        uint64_t *dm = is_x ? d_xm : d_am;
+        int8_t *dsg = is_x ? d_xs : d_as;
+        ok = cudaMemcpyAsync(dm + r0 * L, hm + r0 * L, (r1 - r0) * L * 8, cudaMemcpyHostToDevice,
+                             s1) == cudaSuccess &&
+             cudaMemcpyAsync(dsg + r0, hs + r0, r1 - r0, cudaMemcpyHostToDevice, s1) == cudaSuccess;
+        cudaEvent_t e = new_event();
+        ok = ok && e && cudaEventRecord(e, s1) == cudaSuccess &&
+             cudaStreamWaitEvent(s0, e, 0) == cudaSuccess;
+        if (ok && (rc = launch_k1_range(prm, s0, chunks[c].t0, chunks[c].nt))) { cleanup(); return rc; }
+    }
+    if (ok && (rc = launch_ntt_path(prm, s0, HK_STAGE_COLUMNS))) { cleanup(); return rc; }
+    const int ncy = m >= 64 ? 4 : 1;
+    for (int c = 0; c < ncy && ok; ++c) {
+        int64_t r0 = m * c / ncy / 8 * 8, r1 = c + 1 == ncy ? m : m * (c + 1) / ncy / 8 * 8;
+        if (r1 <= r0) continue;
+        if ((rc = launch_k3_range(prm, s0, r0, r1 - r0))) { cleanup(); return rc; }
+        // y rows of this chunk (Toeplitz writes rows reversed: m-1-r)
+        const int64_t o0 = pl.reverse_out ? m - r1 : r0, o1 = pl.reverse_out ? m - r0 : r1;
+        cudaEvent_t e = new_event();
+        ok = e && cudaEventRecord(e, s0) == cudaSuccess && cudaStreamWaitEvent(s2, e, 0) == cudaSuccess &&
+             cudaMemcpyAsync(y_mag_host + o0 * Ly, d_ym + o0 * Ly, (o1 - o0) * Ly * 8,
+                             cudaMemcpyDeviceToHost, s2) == cudaSuccess &&
+             cudaMemcpyAsync(y_sign_host + o0, d_ys + o0, o1 - o0, cudaMemcpyDeviceToHost, s2) ==
+                 cudaSuccess;
+    }
+    cudaEvent_t ed = new_event();
+    ok = ok && ed && cudaEventRecord(ed, s2) == cudaSuccess && cudaStreamWaitEvent(s0, ed, 0) == cudaSuccess;
     int32_t ds = HK_ECUDA;
-    rc = hk_workspace_status(ws, stream, &ds);
+    rc = ok ? hk_workspace_status(ws, stream, &ds) : HK_ECUDA;
+    cleanup();
     if (rc) return rc;
     return ds;
 }

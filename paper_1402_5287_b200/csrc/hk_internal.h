@@ -49,6 +49,8 @@ struct Params {
     int64_t ldA, ldX, ldY, ldS;  // leading dims (elements) of the transform-domain arrays
     uint64_t hash;
     int32_t diag;                // diagnostics-only switches (HK_K2_DIAG); 0 in production
+    int32_t tile0;               // K1: first tile of this launch (combined [a tiles | x tiles] index)
+    int64_t row0;                // K3: first output row of this launch
     // inputs / outputs (device)
     const uint64_t *a_mag;
     const int8_t *a_sign;
@@ -76,6 +78,12 @@ struct Plan {
 // kernels (hk_ntt.cu)
 int launch_init(const Params &prm, const uint32_t *gens, void *stream);
 int launch_ntt_path(const Params &prm, void *stream, uint32_t stages);
+// partial launches for the pipelined host path: K1 over tiles [tile0, tile0 + ntiles) of the
+// combined [a | x] tile index (8 rows per tile), K3 over output rows [row0, row0 + nrows)
+int k1_tiles_a(const Params &prm);
+int k1_tiles_x(const Params &prm);
+int launch_k1_range(const Params &prm, void *stream, int tile0, int ntiles);
+int launch_k3_range(const Params &prm, void *stream, int64_t row0, int64_t nrows);
 // companion (hk_schoolbook.cu)
 int launch_schoolbook(int kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                       const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,

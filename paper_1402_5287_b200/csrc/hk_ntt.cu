@@ -100,8 +100,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params pr
         if (tid == 0 && blockIdx.x == 0) atomicMin(&prm.hdr->status, (int)HK_EINVAL);
         return;
     }
-    const bool is_x = (int)blockIdx.x >= tiles_a;
-    const int tile = is_x ? (int)blockIdx.x - tiles_a : (int)blockIdx.x;
+    const int bt = (int)blockIdx.x + prm.tile0;
+    const bool is_x = bt >= tiles_a;
+    const int tile = is_x ? bt - tiles_a : bt;
     const uint64_t *mag = is_x ? prm.x_mag : prm.a_mag;
     const int8_t *sgn = is_x ? prm.x_sign : prm.a_sign;
     const int64_t count = is_x ? prm.n : prm.a_count;
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kK3aThreads, 2) k3a_row_intt_crt(Params prm) {
     constexpr int RS = k1_row_stride<LOGN2>();
     extern __shared__ uint32_t sm[];  // [prime][row][RS]
     const int tid = threadIdx.x;
-    const int64_t r0 = (int64_t)blockIdx.x * k3_rows<LOGN2>();
+    const int64_t r0 = prm.row0 + (int64_t)blockIdx.x * k3_rows<LOGN2>();
     const int64_t m = prm.m;
     for (int idx = tid; idx < kNumPrimes * N2 * k3_rows<LOGN2>(); idx += kK3aThreads) {
         const int r = idx % k3_rows<LOGN2>(), cs = idx / k3_rows<LOGN2>();  // cs = kp * N2 + sigma
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
     __shared__ int s_wcarry[kK3Threads / 32];
     __shared__ int s_neg, s_zmin;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t row = blockIdx.x;
+    const int64_t row = prm.row0 + blockIdx.x;
     const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
     uint8_t *sB = reinterpret_cast<uint8_t *>(sP + 4 * Ly);
     {  // zero the slot arrays (positions without a coefficient stay 0)
@@ -526,26 +527,35 @@ int launch_init(const Params &prm, const uint32_t *gens, void *stream) {
 }
 
 template <int LOGN2>
-static int launch_rows(const Params &prm, cudaStream_t st) {
-    const int ga = (int)((prm.a_count + kK1Rows - 1) / kK1Rows);
-    const int gx = (int)((prm.n + kK1Rows - 1) / kK1Rows);
+static int launch_rows(const Params &prm0, cudaStream_t st, int tile0 = 0, int ntiles = -1) {
+    const int ga = (int)((prm0.a_count + kK1Rows - 1) / kK1Rows);
+    const int gx = (int)((prm0.n + kK1Rows - 1) / kK1Rows);
+    if (ntiles < 0) ntiles = ga + gx - tile0;
+    if (ntiles <= 0) return HK_OK;
+    Params prm = prm0;
+    prm.tile0 = tile0;
     const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t) +
                          (size_t)kK1Rows * prm.L * sizeof(uint64_t);
     if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess)
         return HK_ECUDA;
-    k1_slice_rowntt<LOGN2><<<ga + gx, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
+    k1_slice_rowntt<LOGN2><<<ntiles, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();
 }
 
 template <int LOGN2>
-static int launch_rows_inverse(const Params &prm, cudaStream_t st) {
+static int launch_rows_inverse(const Params &prm0, cudaStream_t st, int64_t row0 = 0,
+                               int64_t nrows = -1) {
+    if (nrows < 0) nrows = prm0.m - row0;
+    if (nrows <= 0) return HK_OK;
+    Params prm = prm0;
+    prm.row0 = row0;
     const size_t smem =
         (size_t)kNumPrimes * k3_rows<LOGN2>() * k1_row_stride<LOGN2>() * sizeof(uint32_t);
     if (cudaFuncSetAttribute(k3a_row_intt_crt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
-    const unsigned grid = (unsigned)((prm.m + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
+    const unsigned grid = (unsigned)((nrows + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
     k3a_row_intt_crt<LOGN2><<<grid, kK3aThreads, smem, st>>>(prm);
     return check_launch();
 }
@@ -595,13 +605,35 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
     }
     if (rc) return rc;
     if (!(stages & HK_STAGE_FINISH)) return HK_OK;
+    return launch_k3_range(prm, stream, 0, prm.m);
+}
+
+int k1_tiles_a(const Params &prm) { return (int)((prm.a_count + kK1Rows - 1) / kK1Rows); }
+int k1_tiles_x(const Params &prm) { return (int)((prm.n + kK1Rows - 1) / kK1Rows); }
+
+int launch_k1_range(const Params &prm, void *stream, int tile0, int ntiles) {
+    cudaStream_t st = (cudaStream_t)stream;
     switch (prm.log_n2) {
-#define HK_CASE(LG) case LG: rc = launch_rows_inverse<LG>(prm, st); break;
+#define HK_CASE(LG) case LG: return launch_rows<LG>(prm, st, tile0, ntiles);
+        HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
+}
+
+int launch_k3_range(const Params &prm0, void *stream, int64_t row0, int64_t nrows) {
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = HK_OK;
+    switch (prm0.log_n2) {
+#define HK_CASE(LG) case LG: rc = launch_rows_inverse<LG>(prm0, st, row0, nrows); break;
         HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)
 #undef HK_CASE
         default: return HK_EUNSUPPORTED;
     }
     if (rc) return rc;
+    if (nrows <= 0) return HK_OK;
+    Params prm = prm0;
+    prm.row0 = row0;
     const size_t smem3 = ((size_t)4 * prm.Ly * 8 + prm.Ly + 15) / 16 * 16;
     const int chunk = (prm.Ly + kK3Threads - 1) / kK3Threads;
     switch (chunk) {
@@ -610,7 +642,7 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
         if (cudaFuncSetAttribute(k3b_carry<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
                                  (int)smem3) != cudaSuccess)                                   \
             return HK_ECUDA;                                                                   \
-        k3b_carry<C><<<(unsigned)prm.m, kK3Threads, smem3, st>>>(prm);                         \
+        k3b_carry<C><<<(unsigned)nrows, kK3Threads, smem3, st>>>(prm);                         \
         break;
         HK_CASE(1) HK_CASE(2) HK_CASE(3) HK_CASE(4) HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8)
         HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12) HK_CASE(13) HK_CASE(14) HK_CASE(15)

@@ -107,10 +107,12 @@ def test_rect_windows(hk):
         full_case(hk, 0, n, 3000, seed=m + n, m=m)
 
 
-def test_host_buffer_path(hk):
-    am, asg, xm, xsg = gen.make_inputs(0, 200, 5000, seed=3)
-    ym, ys = hk.matvec_host(0, am, asg, xm, xsg, 5000)
-    assert_same((ym, ys), oracle.matvec(0, 5000, am, asg, xm, xsg), "host path")
+@pytest.mark.parametrize("kind,n", [(0, 200), (1, 203), (2, 128), (2, 77), (0, 5), (1, 1)])
+def test_host_buffer_path(hk, kind, n):
+    """hk_matvec_host: chunked H2D / K1, K2, chunked K3 / D2H pipeline."""
+    am, asg, xm, xsg = gen.make_inputs(kind, n, 5000, seed=3 + n)
+    ym, ys = hk.matvec_host(kind, am, asg, xm, xsg, 5000)
+    assert_same((ym, ys), oracle.matvec(kind, 5000, am, asg, xm, xsg), "host path")
 
 
 def test_workspace_reuse_and_determinism(hk):

@@ -32,8 +32,9 @@ struct ColPlan {
     static_assert(GPT >= 1 && GPT * GL * T == (1 << LOGN), "bottom pass must tile the threads");
 };
 
-// Top forward pass (R = 5, S = N/32, single block) reading the column straight from HBM.
-template <class TW, int LOGN, int T>
+// Top forward pass (R = 5, S = N/32, single block) reading the column straight from HBM
+// (SRC_SMEM = false) or from a shared-memory staging copy (SRC_SMEM = true).
+template <class TW, int LOGN, int T, bool SRC_SMEM = false>
 HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, bool zu,
                                    uint32_t *sm, const uint2 *tw, uint32_t p) {
     constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
@@ -42,7 +43,8 @@ HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, b
 #pragma unroll
         for (int m = 0; m < G; ++m) {
             const int idx = j0 + m * S;
-            v[m] = (!(zu && m >= G / 2) && idx < nsrc) ? __ldcs(src + idx) : 0u;
+            if (SRC_SMEM) v[m] = (!(zu && m >= G / 2) && idx < nsrc) ? src[idx] : 0u;
+            else v[m] = (!(zu && m >= G / 2) && idx < nsrc) ? __ldcs(src + idx) : 0u;
         }
 #pragma unroll
         for (int l = R - 1; l >= 0; --l) {
@@ -145,13 +147,33 @@ HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, uint32_t *__re
     __syncthreads();
 }
 
+// A^ column staged in shared memory by cp.async while X^ is transformed (hides the HBM
+// latency of A^'s top pass); needs N1 more words of smem, so only for N1 <= 16384.
+template <int LOGN1>
+constexpr bool k2_stage_a() { return LOGN1 <= 14; }
+template <int LOGN1>
+constexpr int k2_stage_off() { return (padded_len(1 << LOGN1) + 3) & ~3; }  // 16-byte aligned
+template <int LOGN1>
+constexpr size_t k2_smem_bytes() {
+    return k2_stage_a<LOGN1>() ? (size_t)(k2_stage_off<LOGN1>() + (1 << LOGN1)) * 4
+                               : (size_t)padded_len(1 << LOGN1) * 4;
+}
+
 template <class TW, int LOGN1>
 HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
     using PL = ColPlan<LOGN1>;
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
+    constexpr bool STAGE = k2_stage_a<LOGN1>();
     const int tid = threadIdx.x;
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
     const size_t cidx = (size_t)kp * prm.N2 + sigma;
+    uint32_t *sA = sm + k2_stage_off<LOGN1>();
+    if constexpr (STAGE) {  // issue the A^ column copy now; consumed after X^'s transform
+        const int na = (int)prm.a_count;
+        const int nch = (na < N1 ? na : N1) + 3 >> 2;
+        const uint32_t *g = prm.Ahat + cidx * prm.ldA;
+        for (int c = tid; c < nch; c += T) cp_async16(sA + 4 * c, g + 4 * c);
+    }
 
     // ---- X^: forward, bottom pass kept in registers
     {
@@ -171,7 +193,14 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     // ---- A^: forward; bottom pass + pointwise + first inverse pass in registers
     {
         const int na = (int)prm.a_count;
-        k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm, twf, p);
+        if constexpr (STAGE) {
+            cp_async_wait_all();
+            __syncthreads();
+            k2_dif_top_from_global<TW, LOGN1, T, true>(sA, na, na <= N1 / 2, sm, twf, p);
+        } else {
+            k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm,
+                                                 twf, p);
+        }
         K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     }
 #pragma unroll

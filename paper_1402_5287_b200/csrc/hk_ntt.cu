@@ -563,7 +563,7 @@ static int launch_rows_inverse(const Params &prm0, cudaStream_t st, int64_t row0
 template <int LOGN1>
 static int launch_cols(const Params &prm, cudaStream_t st) {
     const int ncols = kNumPrimes * prm.N2;
-    const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
+    const size_t smem = k2_smem_bytes<LOGN1>();
     if (cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;

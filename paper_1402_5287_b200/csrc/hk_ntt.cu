@@ -83,7 +83,7 @@ constexpr int k1_threads() {
 }
 
 template <int LOGN2>
-__global__ void __launch_bounds__(k1_threads<LOGN2>()) k1_slice_rowntt(Params prm, int tiles_a) {
+__global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params prm, int tiles_a) {
     constexpr int N2 = 1 << LOGN2;
     constexpr int RS = k1_row_stride<LOGN2>();
     constexpr int T = k1_threads<LOGN2>();

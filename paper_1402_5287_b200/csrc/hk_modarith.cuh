@@ -25,6 +25,7 @@ constexpr uint32_t kP[kPrimes] = {2147352577u, 2146959361u, 2146041857u, 2144468
 // Padded shared-memory index: one spare word after every 32 keeps the strided radix passes
 // (stride S = 1..16 between a thread's points) free of bank conflicts.
 HK_DEV int pad(int i) { return i + (i >> 5); }
+HK_DEV unsigned padu(unsigned i) { return i + (i >> 5); }
 __host__ __device__ constexpr int padded_len(int n) { return n + (n >> 5); }
 
 HK_DEV uint32_t red1(uint32_t x, uint32_t p) { return min(x, x - p); }  // [0,2p) -> [0,p)
@@ -116,18 +117,18 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
     constexpr int G = 1 << R;
     constexpr int NG = N / G;
     static_assert(!ZERO_UPPER || S * G == N, "ZERO_UPPER only for the first pass");
-    const int total = batch * NG;
-    for (int gi = tid; gi < total; gi += nthr) {
-        const int b = gi / NG;
-        const int g = gi % NG;
-        const int j0 = g % S;
-        const int B = (g / S) * (S * G);
+    const unsigned total = (unsigned)(batch * NG);
+    for (unsigned gi = tid; gi < total; gi += nthr) {
+        const unsigned b = gi / NG;
+        const unsigned g = gi % NG;
+        const unsigned j0 = g % S;
+        const unsigned B = (g / S) * (S * G);
         uint32_t *base = s + b * rs;
         uint32_t v[G];
 #pragma unroll
         for (int m = 0; m < G; ++m) {
             if (ZERO_UPPER && m >= G / 2) v[m] = 0;
-            else v[m] = base[pad(B + j0 + m * S)];
+            else v[m] = base[padu(B + j0 + m * S)];
         }
 #pragma unroll
         for (int l = R - 1; l >= 0; --l) {
@@ -139,13 +140,13 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
                     bfly1(v[m], v[m + half], p);
                     continue;
                 }
-                const int j = j0 + S * (m & (half - 1));
+                const unsigned j = j0 + S * (m & (half - 1));
                 const uint2 w = TW::ld(tw, S * half + j);
                 gs_bfly(v[m], v[m + half], w, p);
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) base[pad(B + j0 + m * S)] = v[m];
+        for (int m = 0; m < G; ++m) base[padu(B + j0 + m * S)] = v[m];
     }
     __syncthreads();
 }
@@ -157,16 +158,16 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
     constexpr int N = 1 << LOGN;
     constexpr int G = 1 << R;
     constexpr int NG = N / G;
-    const int total = batch * NG;
-    for (int gi = tid; gi < total; gi += nthr) {
-        const int b = gi / NG;
-        const int g = gi % NG;
-        const int j0 = g % S;
-        const int B = (g / S) * (S * G);
+    const unsigned total = (unsigned)(batch * NG);
+    for (unsigned gi = tid; gi < total; gi += nthr) {
+        const unsigned b = gi / NG;
+        const unsigned g = gi % NG;
+        const unsigned j0 = g % S;
+        const unsigned B = (g / S) * (S * G);
         uint32_t *base = s + b * rs;
         uint32_t v[G];
 #pragma unroll
-        for (int m = 0; m < G; ++m) v[m] = base[pad(B + j0 + m * S)];
+        for (int m = 0; m < G; ++m) v[m] = base[padu(B + j0 + m * S)];
 #pragma unroll
         for (int l = 0; l < R; ++l) {
             const int half = 1 << l;
@@ -177,13 +178,13 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
                     bfly1(v[m], v[m + half], p);
                     continue;
                 }
-                const int j = j0 + S * (m & (half - 1));
+                const unsigned j = j0 + S * (m & (half - 1));
                 const uint2 w = TW::ld(tw, S * half + j);
                 ct_bfly(v[m], v[m + half], w, p);
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) base[pad(B + j0 + m * S)] = v[m];
+        for (int m = 0; m < G; ++m) base[padu(B + j0 + m * S)] = v[m];
     }
     __syncthreads();
 }

@@ -291,6 +291,30 @@ def main():
     if sampler:
         sampler.stop()
 
+    # ---- F1 (secondary): fixed A, new x each step (prepared 2-D transform of a)
+    warm = None
+    if rank == 0 and world == 1:
+        A = hk.PreparedMatrix(kind, a, sa, P, n)
+        yb = (torch.empty((n, plan["Ly"]), dtype=torch.int64, device=dev),
+              torch.empty((n,), dtype=torch.int8, device=dev))
+        for _ in range(W):
+            A.matvec(x, sx, out=yb, check=False)
+        torch.cuda.synchronize()
+        w0 = torch.cuda.Event(enable_timing=True)
+        w1 = torch.cuda.Event(enable_timing=True)
+        w0.record(stream)
+        for _ in range(K):
+            A.matvec(x, sx, out=yb, check=False)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        if A.ws.status() != hk.HK_OK:
+            raise SystemExit("bench: prepared-matvec status not OK")
+        wms = w0.elapsed_time(w1) / K
+        warm = {"value": 1000.0 / wms, "unit": UNIT, "ms_per_step": wms,
+                "what": "same matvec with the 2-D transform of a prepared once (hk_prepare_a); "
+                        "per step: x slicing + transforms, pointwise, inverse, CRT, carry"}
+        del A
+
     # ---- e2e through the host-buffer C-ABI call (N = 1 workload per rank)
     e2e = None
     if rank == 0 and not args.no_e2e and world == 1:
@@ -375,6 +399,7 @@ def main():
         "roofline": roof,
         "cpu_baseline": cb,
         "e2e": e2e,
+        "warm_a": warm,
         "gpu_launches": launches_per_step * K,
         "clocks": clocks,
         "library": hk.library_path(),

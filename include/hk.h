@@ -65,8 +65,9 @@ typedef enum {
 
 typedef enum { HK_HANKEL = 0, HK_TOEPLITZ = 1, HK_CIRCULANT = 2 } hk_kind;
 
-/* hk_workspace_size / hk_workspace_init flags */
+/* hk_workspace_size / hk_workspace_init flags (mutually exclusive) */
 #define HK_WS_STAGING 1u   /* also reserve device staging buffers for hk_matvec_host */
+#define HK_WS_PREPARED 2u  /* also reserve room for a prepared 2-D transform of a (hk_prepare_a) */
 
 /* The plan the library chose for a problem (filled by hk_plan; all sizes in elements). */
 typedef struct {
@@ -87,6 +88,7 @@ typedef struct {
     double margin_bits;    /* log2(p1..p5) - log2(2 n Ls (2^w-1)^2) > 0                         */
     uint64_t ws_bytes;     /* workspace bytes without staging                                  */
     uint64_t ws_bytes_staging; /* workspace bytes with HK_WS_STAGING                           */
+    uint64_t ws_bytes_prepared; /* workspace bytes with HK_WS_PREPARED                         */
 } hk_plan_info;
 
 /* L = ceil(P/64) (l = ceil(b / log2 B)); returns -1 if P < 1. */
@@ -180,6 +182,22 @@ int32_t hk_matvec_stages(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t
                          const uint64_t *x_mag, const int8_t *x_sign,
                          uint64_t *y_mag, int8_t *y_sign,
                          void *ws, size_t ws_bytes, void *stream);
+
+/* Fixed-A repeated products (the Lanczos use of the paper): one
+ * matrix, many vectors.  hk_prepare_a validates a, runs the slice-dimension and matrix-index
+ * forward transforms of a once and keeps the full 2-D transform of a in the workspace (which must
+ * have been sized and initialised with HK_WS_PREPARED for the same kind, m, n, P); the data
+ * status of a is then readable with hk_workspace_status.  hk_matvec_prepared computes y for a new
+ * x with only x's transforms, the pointwise product and the inverse (2 instead of 3 column
+ * transforms, and no slicing of a).  If hk_prepare_a has not run on ws, the status of the call is
+ * HK_EINVAL.  Shapes/kinds as hk_matvec_host; DEVICE pointers; asynchronous on `stream`. */
+int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P,
+                     const uint64_t *a_mag, const int8_t *a_sign,
+                     void *ws, size_t ws_bytes, void *stream);
+int32_t hk_matvec_prepared(int32_t kind, int64_t m, int64_t n, int32_t P,
+                           const uint64_t *x_mag, const int8_t *x_sign,
+                           uint64_t *y_mag, int8_t *y_sign,
+                           void *ws, size_t ws_bytes, void *stream);
 
 /* Companion A6: direct schoolbook limb-product matvec on the GPU, no
  * transform: y_i = sum_j A_{idx(i,j)} X_j with 32-bit limb products and wide column sums.

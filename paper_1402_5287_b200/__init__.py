@@ -23,6 +23,7 @@ from ._build import LIB as _LIB_PATH
 HK_OK, HK_EINVAL, HK_ERANGE, HK_ENOMEM, HK_EUNSUPPORTED, HK_ECUDA = 0, -1, -2, -3, -4, -5
 HANKEL, TOEPLITZ, CIRCULANT = 0, 1, 2
 WS_STAGING = 1
+WS_PREPARED = 2
 
 
 class HKError(RuntimeError):
@@ -38,7 +39,7 @@ class PlanInfo(ctypes.Structure):
                 ("Ls", ctypes.c_int32), ("log_n2", ctypes.c_int32), ("log_n1", ctypes.c_int32),
                 ("cyclic", ctypes.c_int32), ("fold", ctypes.c_int32),
                 ("margin_bits", ctypes.c_double), ("ws_bytes", ctypes.c_uint64),
-                ("ws_bytes_staging", ctypes.c_uint64)]
+                ("ws_bytes_staging", ctypes.c_uint64), ("ws_bytes_prepared", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -67,6 +68,8 @@ def _load():
         "hk_matvec_stages": (i32, [i32, i64, i64, i32, ctypes.c_uint32, vp, vp, vp, vp, vp, vp,
                                    vp, sz, vp]),
         "hk_karatsuba_workspace_size": (i32, [i64, i32, i32, ctypes.POINTER(sz)]),
+        "hk_prepare_a": (i32, [i32, i64, i64, i32, vp, vp, vp, sz, vp]),
+        "hk_matvec_prepared": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
@@ -81,7 +84,7 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_workspace_init", "hk_workspace_status", "hk_hankel_matvec", "hk_toeplitz_matvec",
             "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host",
             "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
-            "hk_karatsuba_matvec")
+            "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -278,6 +281,43 @@ class Problem:
 
     def status(self, stream=None) -> int:
         return self.ws.status(stream)
+
+
+class PreparedMatrix:
+    """F1 (fixed-A repeated products, the paper's Lanczos use P:32-36): the 2-D transform of a is
+    computed once (hk_prepare_a) and reused by every matvec(x) (hk_matvec_prepared)."""
+
+    def __init__(self, kind, a_mag, a_sign, P, n, m=None, stream=None, check=True):
+        import torch
+        self.kind, self.P, self.n = int(kind), int(P), int(n)
+        self.m = self.n if m is None else int(m)
+        L = limbs(P)
+        na = (self.n if kind == CIRCULANT else self.m + self.n - 1)
+        self.a = (a_mag, a_sign)
+        pa = _dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag")
+        ps = _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign")
+        self.ws = Workspace(kind, self.n, P, m=self.m, flags=WS_PREPARED, stream=stream)
+        _check(_lib.hk_prepare_a(self.kind, self.m, self.n, self.P, pa, ps, self.ws.ptr,
+                                 self.ws.nbytes, _stream_ptr(stream)), "hk_prepare_a")
+        if check:
+            _check(self.ws.status(stream), "hk_prepare_a data status")
+
+    def matvec(self, x_mag, x_sign, out=None, stream=None, check=True):
+        import torch
+        L, Ly = limbs(self.P), out_limbs(self.P)
+        px = _dev_ptr(x_mag, _mag_dtypes(), (self.n, L), "x_mag")
+        pxs = _dev_ptr(x_sign, (torch.int8,), (self.n,), "x_sign")
+        if out is None:
+            out = (torch.empty((self.m, Ly), dtype=x_mag.dtype, device=x_mag.device),
+                   torch.empty((self.m,), dtype=torch.int8, device=x_mag.device))
+        py = _dev_ptr(out[0], _mag_dtypes(), (self.m, Ly), "y_mag")
+        pys = _dev_ptr(out[1], (torch.int8,), (self.m,), "y_sign")
+        _check(_lib.hk_matvec_prepared(self.kind, self.m, self.n, self.P, px, pxs, py, pys,
+                                       self.ws.ptr, self.ws.nbytes, _stream_ptr(stream)),
+               "hk_matvec_prepared")
+        if check:
+            _check(self.ws.status(stream), "hk_matvec_prepared data status")
+        return out
 
 
 def schoolbook_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, stream=None):

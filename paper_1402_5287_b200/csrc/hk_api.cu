@@ -170,9 +170,14 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     pl->st_ymag = off;  off = align256(off + (size_t)m * Ly * 8);
     pl->st_ysign = off; off = align256(off + (size_t)m);
     pl->off_end_staging = off;
+    // HK_WS_PREPARED: the 2-D transform of a right after the base layout
+    pl->off_AT = pl->off_end;
+    pl->off_end_prepared = align256(pl->off_AT + (size_t)kNumPrimes * N2 * N1 * 4);
     in.ws_bytes = pl->off_end;
     in.ws_bytes_staging = pl->off_end_staging;
-    (void)flags;
+    in.ws_bytes_prepared = pl->off_end_prepared;
+    if ((flags & HK_WS_STAGING) && (flags & HK_WS_PREPARED)) return HK_EINVAL;
+    if (flags & ~(HK_WS_STAGING | HK_WS_PREPARED)) return HK_EINVAL;
     return HK_OK;
 }
 
@@ -304,7 +309,8 @@ int32_t hk_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_
     Plan pl;
     int rc = make_plan(kind, m, n, P, flags, &pl);
     if (rc) return rc;
-    *bytes = (flags & HK_WS_STAGING) ? pl.info.ws_bytes_staging : pl.info.ws_bytes;
+    *bytes = (flags & HK_WS_STAGING) ? pl.info.ws_bytes_staging
+             : (flags & HK_WS_PREPARED) ? pl.info.ws_bytes_prepared : pl.info.ws_bytes;
     return HK_OK;
 }
 
@@ -314,7 +320,8 @@ int32_t hk_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_
     Plan pl;
     int rc = make_plan(kind, m, n, P, flags, &pl);
     if (rc) return rc;
-    const size_t need = (flags & HK_WS_STAGING) ? pl.info.ws_bytes_staging : pl.info.ws_bytes;
+    const size_t need = (flags & HK_WS_STAGING) ? pl.info.ws_bytes_staging
+                        : (flags & HK_WS_PREPARED) ? pl.info.ws_bytes_prepared : pl.info.ws_bytes;
     if (ws_bytes < need) return HK_ENOMEM;
     Params prm;
     fill_params(pl, ws, &prm);
@@ -468,6 +475,57 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
     cleanup();
     if (rc) return rc;
     return ds;
+}
+
+int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
+                     const int8_t *a_sign, void *ws, size_t ws_bytes, void *stream) {
+    if (!a_mag || !a_sign || !ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
+    if (rc) return rc;
+    if (ws_bytes < pl.info.ws_bytes_prepared) return HK_ENOMEM;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    prm.a_mag = a_mag; prm.a_sign = a_sign;
+    prm.AT = (uint32_t *)((char *)ws + pl.off_AT);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, 2 * sizeof(int32_t), st) != cudaSuccess)  // + a_ready
+        return HK_ECUDA;
+    if ((rc = launch_k1_range(prm, stream, 0, k1_tiles_a(prm)))) return rc;
+    if ((rc = launch_k2_mode(prm, stream, 1))) return rc;
+    const int32_t one = 1;  // a_ready = 1 (stream-ordered after the transforms)
+    if (cudaMemsetAsync(&prm.hdr->a_ready, 0, sizeof(int32_t), st) != cudaSuccess ||
+        cudaMemsetAsync(&prm.hdr->a_ready, one, 1, st) != cudaSuccess)
+        return HK_ECUDA;
+    return HK_OK;
+}
+
+int32_t hk_matvec_prepared(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *x_mag,
+                           const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *ws,
+                           size_t ws_bytes, void *stream) {
+    if (!x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0)
+        return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
+    if (rc) return rc;
+    if (ws_bytes < pl.info.ws_bytes_prepared) return HK_ENOMEM;
+    const size_t Ly = pl.info.Ly, L = pl.info.L;
+    if (overlaps(y_mag, (size_t)m * Ly * 8, x_mag, (size_t)n * L * 8) ||
+        overlaps(y_sign, (size_t)m, x_sign, (size_t)n) ||
+        overlaps(y_mag, (size_t)m * Ly * 8, ws, pl.info.ws_bytes_prepared) ||
+        overlaps(y_sign, (size_t)m, ws, pl.info.ws_bytes_prepared))
+        return HK_EINVAL;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    prm.x_mag = x_mag; prm.x_sign = x_sign; prm.y_mag = y_mag; prm.y_sign = y_sign;
+    prm.AT = (uint32_t *)((char *)ws + pl.off_AT);
+    prm.need_a_ready = 1;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    const int ga = k1_tiles_a(prm);
+    if ((rc = launch_k1_range(prm, stream, ga, k1_tiles_x(prm)))) return rc;
+    if ((rc = launch_k2_mode(prm, stream, 2))) return rc;
+    return launch_k3_range(prm, stream, 0, m);
 }
 
 int32_t hk_matvec_stages(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t stages,

@@ -33,7 +33,8 @@ struct WsHeader {  // first 256 bytes of a workspace
     uint64_t magic;
     uint64_t hash;
     int32_t status;
-    int32_t pad_[59];
+    int32_t a_ready;   // 1 after hk_prepare_a wrote the 2-D transform of a into AT
+    int32_t pad_[58];
 };
 
 // Everything a launch needs, passed by value.
@@ -62,6 +63,8 @@ struct Params {
     WsHeader *hdr;
     const uint2 *tw;             // per prime: [N2 forward table | N1 forward table]
     uint32_t *Ahat, *Xhat, *Yhat, *Yres;
+    uint32_t *AT;                // prepared 2-D transform of a (HK_WS_PREPARED), or null
+    int32_t need_a_ready;        // K1 (x tiles): require hdr->a_ready
     PrimeConsts pc[kNumPrimes];
     GarnerConsts gc;
 };
@@ -73,6 +76,7 @@ struct Plan {
     int64_t ldA, ldX, ldY, ldS;
     size_t off_tw, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
     size_t st_amag, st_asign, st_xmag, st_xsign, st_ymag, st_ysign;
+    size_t off_AT, off_end_prepared;
 };
 
 // kernels (hk_ntt.cu)
@@ -84,6 +88,9 @@ int k1_tiles_a(const Params &prm);
 int k1_tiles_x(const Params &prm);
 int launch_k1_range(const Params &prm, void *stream, int tile0, int ntiles);
 int launch_k3_range(const Params &prm, void *stream, int64_t row0, int64_t nrows);
+// K2 variants: 0 = full (X^ and A^ transforms), 1 = prepare (A^ transform -> AT),
+// 2 = prepared (X^ transform x AT, inverse)
+int launch_k2_mode(const Params &prm, void *stream, int mode);
 // companion (hk_schoolbook.cu)
 int launch_schoolbook(int kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                       const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,

@@ -233,15 +233,96 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     }
 }
 
+// Inverse passes above the bottom one, output to Y^ (shared by the full and prepared bodies).
+template <class TW, int LOGN1>
+HK_DEV void k2_inverse_tail(const Params &prm, uint32_t *sm, const uint2 *twf, uint32_t p,
+                            size_t cidx) {
+    using PL = ColPlan<LOGN1>;
+    constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL;
+    K2DitMiddle<TW, LOGN1, RL>::run(sm, twf, p);
+    uint32_t *yc = prm.Yhat + cidx * prm.ldY;
+    const int mrows = (int)prm.m, off = (int)prm.out_off;
+    if (!prm.fold) {
+        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, false);
+    } else {
+        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, true);
+        const int nn = (int)prm.n;
+        for (int i = threadIdx.x; i < mrows; i += T) {
+            const uint32_t v = sm[pad((N1 - (off + i)) & (N1 - 1))];
+            yc[i] = addm(v, sm[pad((N1 - (off + i + nn)) & (N1 - 1))], p);
+        }
+        __syncthreads();
+    }
+}
+
+// F1 prepare: A^'s forward column transform only, stored to AT in the bottom-pass register
+// layout AT[col][k GL + m][T] (coalesced, read back by the same thread slot in k2_prepared).
+template <class TW, int LOGN1>
+HK_DEV void k2_prepare_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
+    using PL = ColPlan<LOGN1>;
+    constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
+    const int tid = threadIdx.x;
+    const uint32_t p = prm.pc[kp].p;
+    const size_t cidx = (size_t)kp * prm.N2 + sigma;
+    const int na = (int)prm.a_count;
+    k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm, twf, p);
+    K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
+    uint32_t *at = prm.AT + cidx * N1;
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+        const int g = tid + k * T;
+        uint32_t v[GL];
+#pragma unroll
+        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL + m)];
+        dif_bottom_regs<TW, RL>(v, twf, p);
+#pragma unroll
+        for (int m = 0; m < GL; ++m) at[(k * GL + m) * T + tid] = v[m];
+    }
+}
+
+// F1 prepared matvec: X^ forward, pointwise with the stored A^ transform, inverse.
+template <class TW, int LOGN1>
+HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
+    using PL = ColPlan<LOGN1>;
+    constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
+    const int tid = threadIdx.x;
+    const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
+    const size_t cidx = (size_t)kp * prm.N2 + sigma;
+    const int nx = (int)prm.n;
+    k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx, nx <= N1 / 2, sm, twf, p);
+    K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
+    const uint32_t *at = prm.AT + cidx * N1;
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+        const int g = tid + k * T;
+        uint32_t v[GL], av[GL];
+#pragma unroll
+        for (int m = 0; m < GL; ++m) av[m] = __ldcs(at + (k * GL + m) * T + tid);
+#pragma unroll
+        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL + m)];
+        dif_bottom_regs<TW, RL>(v, twf, p);
+#pragma unroll
+        for (int m = 0; m < GL; ++m) v[m] = mont(av[m], v[m], p, pneg);
+        dit_bottom_regs<TW, RL>(v, twf, p);
+#pragma unroll
+        for (int m = 0; m < GL; ++m) sm[pad(g * GL + m)] = v[m];
+    }
+    __syncthreads();
+    k2_inverse_tail<TW, LOGN1>(prm, sm, twf, p, cidx);
+}
+
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
+// MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT).
 // TW = TwConst is a diagnostics-only variant (HK_K2_DIAG=1; wrong results).
-template <int LOGN1, class TW = TwGlobal>
+template <int LOGN1, class TW = TwGlobal, int MODE = 0>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), 1) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
     const int col = blockIdx.x;
     const int kp = col >> prm.log_n2;
     const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1) + prm.N2;
-    k2_column_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
+    if constexpr (MODE == 0) k2_column_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
+    else if constexpr (MODE == 1) k2_prepare_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
+    else k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
 }
 
 }  // namespace hk

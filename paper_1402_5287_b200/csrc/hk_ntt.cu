@@ -62,6 +62,7 @@ __global__ void k0_init(Params prm, uint2 *tw, uint32_t g0, uint32_t g1, uint32_
         prm.hdr->magic = kWsMagic;
         prm.hdr->hash = prm.hash;
         prm.hdr->status = HK_OK;
+        prm.hdr->a_ready = 0;
     }
 }
 
@@ -102,6 +103,10 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
     }
     const int bt = (int)blockIdx.x + prm.tile0;
     const bool is_x = bt >= tiles_a;
+    if (prm.need_a_ready && prm.hdr->a_ready != 1) {
+        if (tid == 0) atomicMin(&prm.hdr->status, (int)HK_EINVAL);
+        return;
+    }
     const int tile = is_x ? bt - tiles_a : bt;
     const uint64_t *mag = is_x ? prm.x_mag : prm.a_mag;
     const int8_t *sgn = is_x ? prm.x_sign : prm.a_sign;
@@ -606,6 +611,31 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
     if (rc) return rc;
     if (!(stages & HK_STAGE_FINISH)) return HK_OK;
     return launch_k3_range(prm, stream, 0, prm.m);
+}
+
+template <int LOGN1, int MODE>
+static int launch_cols_mode(const Params &prm, cudaStream_t st) {
+    const int ncols = kNumPrimes * prm.N2;
+    const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
+    if (cudaFuncSetAttribute(k2_column<LOGN1, TwGlobal, MODE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    k2_column<LOGN1, TwGlobal, MODE><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
+    return check_launch();
+}
+
+int launch_k2_mode(const Params &prm, void *stream, int mode) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (mode == 0) return launch_ntt_path(prm, stream, HK_STAGE_COLUMNS);
+    switch (prm.log_n1) {
+#define HK_CASE(LG)                                                                   \
+    case LG:                                                                          \
+        return mode == 1 ? launch_cols_mode<LG, 1>(prm, st) : launch_cols_mode<LG, 2>(prm, st);
+        HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12)
+        HK_CASE(13) HK_CASE(14) HK_CASE(15)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
 }
 
 int k1_tiles_a(const Params &prm) { return (int)((prm.a_count + kK1Rows - 1) / kK1Rows); }

@@ -88,7 +88,10 @@ def test_workspace_size_monotone():
     a = hk.workspace_size(0, 1000, 33216)
     b = hk.workspace_size(0, 2000, 33216)
     s = hk.workspace_size(0, 1000, 33216, flags=hk.WS_STAGING)
-    assert 0 < a < b and s > a
+    pr = hk.workspace_size(0, 1000, 33216, flags=hk.WS_PREPARED)
+    assert 0 < a < b and s > a and pr > a
+    with pytest.raises(hk.HKError):  # staging and prepared are mutually exclusive
+        hk.workspace_size(0, 1000, 33216, flags=hk.WS_STAGING | hk.WS_PREPARED)
 
 
 def test_null_pointer_arguments_rejected_synchronously():

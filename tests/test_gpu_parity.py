@@ -272,3 +272,33 @@ def test_karatsuba_carry_stress_and_c2_rows(hk):
     rows = np.array([0, 1, 511, 1022, 1023], dtype=np.int64)
     wm, ws_ = oracle.matvec(0, 33216, am, asg, xm, xsg, rows=rows)
     assert_same((got[0][rows], got[1][rows]), (wm, ws_), "karatsuba C2 rows")
+
+
+# ---------------------------------------------------------------------------------------------
+# F1: fixed-A repeated products (prepared transform of a)
+@pytest.mark.parametrize("kind,n,P", [(0, 64, 3328), (1, 100, 2000), (2, 128, 1000), (2, 77, 700),
+                                      (0, 1, 64), (0, 1000, 33216)])
+def test_prepared_matrix_many_vectors(hk, kind, n, P):
+    am, asg, _, _ = gen.make_inputs(kind, n, P, seed=31 + n)
+    A = hk.PreparedMatrix(kind, *hk.to_device(am, asg), P, n)
+    for v in range(3):
+        xm, xsg = gen.uniform(100 + v, 1, n, P)
+        got = hk.to_host(*A.matvec(*hk.to_device(xm, xsg)))
+        if n <= 200:
+            want = oracle.matvec(kind, P, am, asg, xm, xsg)
+            assert_same(got, want, f"prepared kind={kind} n={n} v={v}")
+        else:
+            fp.check(kind, am, asg, xm, xsg, *got)
+
+
+def test_prepared_requires_prepare(hk):
+    P, n = 128, 10
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=3)
+    ws = hk.Workspace(0, n, P, flags=hk.WS_PREPARED)  # initialised, never prepared
+    x, sx = hk.to_device(xm, xsg)
+    y = torch.empty((n, gen.n_out_limbs(P)), dtype=torch.int64, device="cuda")
+    ysg = torch.empty(n, dtype=torch.int8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    rc = hk._lib.hk_matvec_prepared(0, n, n, P, x.data_ptr(), sx.data_ptr(), y.data_ptr(),
+                                    ysg.data_ptr(), ws.ptr, ws.nbytes, s)
+    assert rc == hk.HK_OK and ws.status() == hk.HK_EINVAL

@@ -181,7 +181,14 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
         const uint32_t p = prm.pc[kp].p;
         const uint32_t *F = is_x ? prm.pc[kp].fx : prm.pc[kp].fa;
         const uint32_t *Fq = is_x ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
-        const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
+        // this prime's N2 twiddle table -> smem (the limb staging area is free after extraction)
+        uint2 *tw = reinterpret_cast<uint2 *>(slimb);
+        __syncthreads();
+        {
+            const uint4 *src = reinterpret_cast<const uint4 *>(prm.tw + (size_t)kp * (prm.N2 + prm.N1));
+            for (int i = tid; i < N2 / 2; i += T) reinterpret_cast<uint4 *>(tw)[i] = src[i];
+        }
+        __syncthreads();
         if (act) {
             uint32_t v[G1];
 #pragma unroll
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
             // top stage (h = N2/2) with a zero upper half: (u, 0) -> (u, u W)
 #pragma unroll
             for (int m = 0; m < H1; ++m) {
-                const uint2 wv = TwGlobal::ld(tw, S1 * H1 + j0 + S1 * m);
+                const uint2 wv = TwShared::ld(tw, S1 * H1 + j0 + S1 * m);
                 v[m + H1] = red1(shoup(v[m], wv.x, wv.y, p), p);
             }
 #pragma unroll
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
 #pragma unroll
                 for (int m = 0; m < G1; ++m) {
                     if (m & half) continue;
-                    const uint2 wv = TwGlobal::ld(tw, S1 * half + j0 + S1 * (m & (half - 1)));
+                    const uint2 wv = TwShared::ld(tw, S1 * half + j0 + S1 * (m & (half - 1)));
                     gs_bfly(v[m], v[m + half], wv, p);
                 }
             }
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
         constexpr int REM = LOGN2 - R1;          // stages left after the top pass
         constexpr int RB = REM < 5 ? REM : 5;    // bottom pass (S = 1) radix
         if constexpr (REM > RB)
-            dif_pass<TwGlobal, LOGN2, REM - RB, (1 << RB), false>(sm, kK1Rows, RS, tw, p, tid, T);
+            dif_pass<TwShared, LOGN2, REM - RB, (1 << RB), false>(sm, kK1Rows, RS, tw, p, tid, T);
         // ---- bottom pass in registers, stored straight to [prime][sigma][row]; lanes cover
         // 8 rows x 4 groups so every store instruction writes full 32-byte row segments
         // (x rows reversed: matrix index n-1-row)
@@ -227,7 +234,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
             uint32_t v[GB];
 #pragma unroll
             for (int m = 0; m < GB; ++m) v[m] = sm[rr * RS + pad(g * GB + m)];
-            dif_bottom_regs<TwGlobal, RB>(v, tw, p);
+            dif_bottom_regs<TwShared, RB>(v, tw, p);
             const int64_t orow = r0 + rr;
             if (orow < count) {
                 const int64_t pos = rev ? (count - 1 - orow) : orow;
@@ -539,8 +546,10 @@ static int launch_rows(const Params &prm0, cudaStream_t st, int tile0 = 0, int n
     if (ntiles <= 0) return HK_OK;
     Params prm = prm0;
     prm.tile0 = tile0;
+    const size_t limb_bytes = (size_t)kK1Rows * prm.L * sizeof(uint64_t);
+    const size_t tab_bytes = (size_t)(1 << LOGN2) * sizeof(uint2);  // reuses the limb area
     const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t) +
-                         (size_t)kK1Rows * prm.L * sizeof(uint64_t);
+                         (limb_bytes > tab_bytes ? limb_bytes : tab_bytes);
     if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess)
         return HK_ECUDA;

@@ -229,6 +229,14 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
             c.fx_q[d] = shoup_q(c.fx[d], p);
         }
     }
+    {
+        Big Mb = big_from(1);
+        for (int k = 0; k < kNumPrimes; ++k) {
+            Mb = big_mul(Mb, big_from(kPrimesHost[k]));
+            prm->gc.half[k] = (kPrimesHost[k] - 1) / 2;
+        }
+        for (int k = 0; k < kNumPrimes; ++k) prm->gc.M[k] = k < (int)Mb.size() ? Mb[k] : 0u;
+    }
     for (int j = 0; j < kNumPrimes; ++j)
         for (int k = 0; k < kNumPrimes; ++k) {
             if (j >= k) continue;

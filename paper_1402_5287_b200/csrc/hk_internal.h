@@ -27,6 +27,8 @@ struct PrimeConsts {
 struct GarnerConsts {
     uint32_t inv[kNumPrimes][kNumPrimes];    // p_j^-1 mod p_k, j < k
     uint32_t inv_q[kNumPrimes][kNumPrimes];  // Shoup quotients
+    uint32_t half[kNumPrimes];               // (p_k - 1) / 2: mixed-radix digits of (M-1)/2
+    uint32_t M[kNumPrimes];                  // M = p0 p1 p2 p3 p4 as 32-bit words
 };
 
 struct WsHeader {  // first 256 bytes of a workspace

@@ -256,34 +256,56 @@ template <int LOGN2>
 constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : 4; }  // 5 x rows x N2 words in smem
 constexpr int kK3aThreads = 320;  // 5 primes x 4 rows x 32 groups = 2 groups per thread
 
-HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint64_t &c0, uint64_t &c1,
-                   uint64_t &c2) {
-    int32_t v[kNumPrimes];
+// Garner CRT with standard mixed-radix digits u_k in [0, p_k):
+//   C' = u0 + p0 (u1 + p1 (u2 + p2 (u3 + p3 u4)))  in [0, M),  M = p0 p1 p2 p3 p4 < 2^155,
+// evaluated in 32-bit words; the symmetric value is C' - M when C' > (M-1)/2, which holds iff the
+// digit vector (u4..u0) exceeds ((p4-1)/2 .. (p0-1)/2) lexicographically.  Output: C as five
+// 32-bit two's-complement words (bit 159 = sign; |C| < M/2 < 2^154).
+HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint32_t (&cw)[kNumPrimes]) {
+    uint32_t u[kNumPrimes];
 #pragma unroll
     for (int k = 0; k < kNumPrimes; ++k) {
         const uint32_t p = prm.pc[k].p;
         uint32_t t = r[k];
 #pragma unroll
         for (int j = 0; j < k; ++j) {
-            const uint32_t vm = v[j] < 0 ? (uint32_t)(v[j] + (int32_t)p) : (uint32_t)v[j];
-            t = subm(t, vm, p);
+            t = subm(t, red1(u[j], p), p);  // u_j < p_j < 2 p_k
             t = red1(shoup(t, prm.gc.inv[j][k], prm.gc.inv_q[j][k], p), p);
         }
-        v[k] = t > (p >> 1) ? (int32_t)(t - p) : (int32_t)t;
+        u[k] = t;
     }
-    // C = v0 + p0 (v1 + p1 (v2 + p2 (v3 + p3 v4)))
-    __int128 acc = v[4];
-    acc = acc * (__int128)prm.pc[3].p + v[3];
-    acc = acc * (__int128)prm.pc[2].p + v[2];
-    acc = acc * (__int128)prm.pc[1].p + v[1];  // |acc| < 2^124
-    const uint64_t p0 = prm.pc[0].p;
-    const uint64_t alo = (uint64_t)acc;
-    const __int128 ahi = acc >> 64;                                  // signed, |ahi| < 2^60
-    const __int128 s = (__int128)((unsigned __int128)alo * p0) + v[0];  // in (-2^31, 2^95)
-    const __int128 H = ahi * (__int128)p0 + (s >> 64);
-    c0 = (uint64_t)s;
-    c1 = (uint64_t)H;
-    c2 = (uint64_t)(H >> 64);
+    uint32_t a0, a1, a2, a3, a4;
+    uint64_t t = (uint64_t)u[4] * prm.pc[3].p + u[3];
+    a0 = (uint32_t)t; a1 = (uint32_t)(t >> 32);
+    t = (uint64_t)a0 * prm.pc[2].p + u[2]; a0 = (uint32_t)t;
+    t = (uint64_t)a1 * prm.pc[2].p + (t >> 32); a1 = (uint32_t)t; a2 = (uint32_t)(t >> 32);
+    t = (uint64_t)a0 * prm.pc[1].p + u[1]; a0 = (uint32_t)t;
+    t = (uint64_t)a1 * prm.pc[1].p + (t >> 32); a1 = (uint32_t)t;
+    t = (uint64_t)a2 * prm.pc[1].p + (t >> 32); a2 = (uint32_t)t; a3 = (uint32_t)(t >> 32);
+    t = (uint64_t)a0 * prm.pc[0].p + u[0]; a0 = (uint32_t)t;
+    t = (uint64_t)a1 * prm.pc[0].p + (t >> 32); a1 = (uint32_t)t;
+    t = (uint64_t)a2 * prm.pc[0].p + (t >> 32); a2 = (uint32_t)t;
+    t = (uint64_t)a3 * prm.pc[0].p + (t >> 32); a3 = (uint32_t)t; a4 = (uint32_t)(t >> 32);
+    // sign: lexicographic (u4, u3, u2, u1, u0) > (h4, h3, h2, h1, h0)
+    bool neg = false, eq = true;
+#pragma unroll
+    for (int k = kNumPrimes - 1; k >= 0; --k) {
+        const uint32_t h = prm.gc.half[k];
+        neg = neg || (eq && u[k] > h);
+        eq = eq && u[k] == h;
+    }
+    if (neg) {  // C = C' - M (160-bit)
+        const uint64_t lo = ((uint64_t)a1 << 32 | a0), mlo = ((uint64_t)prm.gc.M[1] << 32 | prm.gc.M[0]);
+        const uint64_t mid = ((uint64_t)a3 << 32 | a2), mmid = ((uint64_t)prm.gc.M[3] << 32 | prm.gc.M[2]);
+        const uint64_t rlo = lo - mlo;
+        const uint64_t b1 = lo < mlo;
+        const uint64_t rmid = mid - mmid - b1;
+        const uint32_t b2 = (mid < mmid) | ((mid == mmid) & (uint32_t)b1);
+        a4 = a4 - prm.gc.M[4] - b2;
+        a0 = (uint32_t)rlo; a1 = (uint32_t)(rlo >> 32);
+        a2 = (uint32_t)rmid; a3 = (uint32_t)(rmid >> 32);
+    }
+    cw[0] = a0; cw[1] = a1; cw[2] = a2; cw[3] = a3; cw[4] = a4;
 }
 
 template <int LOGN2, int R, int S>
@@ -356,14 +378,11 @@ __global__ void __launch_bounds__(kK3aThreads, 2) k3a_row_intt_crt(Params prm) {
         const int pos = pad((N2 - t) & (N2 - 1));  // slice index negated (forward-root DIT)
 #pragma unroll
         for (int kp = 0; kp < kNumPrimes; ++kp) res[kp] = sm[(kp * k3_rows<LOGN2>() + r) * RS + pos];
-        uint64_t c0, c1, c2;
-        garner(res, prm, c0, c1, c2);
+        uint32_t cw[kNumPrimes];
+        garner(res, prm, cw);
         uint32_t *dst = prm.Yres + row * kNumPrimes * prm.ldS + t;
-        dst[0] = (uint32_t)c0;
-        dst[prm.ldS] = (uint32_t)(c0 >> 32);
-        dst[2 * prm.ldS] = (uint32_t)c1;
-        dst[3 * prm.ldS] = (uint32_t)(c1 >> 32);
-        dst[4 * prm.ldS] = (uint32_t)c2;  // bits 128..159; |C| < 2^155, sign in bit 159
+#pragma unroll
+        for (int k = 0; k < kNumPrimes; ++k) dst[k * prm.ldS] = cw[k];  // bit 159 = sign
     }
 }
 

@@ -236,7 +236,7 @@ def main():
             e[2].record(stream)
             prob.run(hk.STAGE_FINISH)
             e[3].record(stream)
-        launches_per_step = 5  # K1 (a), K1 (x), K2, K3a, K3b
+        launches_per_step = 3  # K1 (a and x tiles), K2, K3
     else:
         from paper_1402_5287_b200 import dist as hkdist
         sh = hkdist.ShardedHankel(a, sa, x, sx, P)

@@ -20,6 +20,9 @@ import numpy as np
 
 from ._build import LIB as _LIB_PATH
 
+# dev A/B only: load an alternative in-tree build of the same library (scripts/gpu_ab.sh)
+_LIB_PATH = os.environ.get("HK_LIB_VARIANT", _LIB_PATH)
+
 HK_OK, HK_EINVAL, HK_ERANGE, HK_ENOMEM, HK_EUNSUPPORTED, HK_ECUDA = 0, -1, -2, -3, -4, -5
 HANKEL, TOEPLITZ, CIRCULANT = 0, 1, 2
 WS_STAGING = 1

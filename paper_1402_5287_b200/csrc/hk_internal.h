@@ -15,8 +15,8 @@ constexpr int kMinLogN1 = 6;
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
-constexpr int kK3Threads = 128;                         // carry block (one output row)
-constexpr int kK3MaxChunk = 17;                         // limbs per thread -> Ly <= 2176
+constexpr int kK3Threads = 320;                         // K3 block (carry: one output row at a time)
+constexpr int kK3MaxChunk = 7;                          // limbs per thread -> Ly <= 2240
 
 struct PrimeConsts {
     uint32_t p, pneg;          // modulus, -p^-1 mod 2^32 (Montgomery)

@@ -16,10 +16,22 @@
 
 namespace hk {
 
+#ifndef HK_K2_T14
+#define HK_K2_T14 512  // threads per CTA at N1 = 2^14
+#endif
+#ifndef HK_K2_MINB14
+#define HK_K2_MINB14 1  // resident CTAs per SM at N1 = 2^14
+#endif
+#ifndef HK_K2_STAGE14
+#define HK_K2_STAGE14 1  // stage the A^ column in smem by cp.async at N1 = 2^14
+#endif
 template <int LOGN1>
 constexpr int k2_threads() {
+    if (LOGN1 == 14) return HK_K2_T14;
     return (1 << LOGN1) / 32 < 32 ? 32 : ((1 << LOGN1) / 32 > 512 ? 512 : (1 << LOGN1) / 32);
 }
+template <int LOGN1>
+constexpr int k2_min_blocks() { return LOGN1 == 14 ? HK_K2_MINB14 : 1; }
 
 template <int LOGN>
 struct ColPlan {
@@ -150,7 +162,7 @@ HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, uint32_t *__re
 // A^ column staged in shared memory by cp.async while X^ is transformed (hides the HBM
 // latency of A^'s top pass); needs N1 more words of smem, so only for N1 <= 16384.
 template <int LOGN1>
-constexpr bool k2_stage_a() { return LOGN1 <= 14; }
+constexpr bool k2_stage_a() { return LOGN1 < 14 || (LOGN1 == 14 && HK_K2_STAGE14); }
 template <int LOGN1>
 constexpr int k2_stage_off() { return (padded_len(1 << LOGN1) + 3) & ~3; }  // 16-byte aligned
 template <int LOGN1>
@@ -315,7 +327,7 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
 // MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT).
 // TW = TwConst is a diagnostics-only variant (HK_K2_DIAG=1; wrong results).
 template <int LOGN1, class TW = TwGlobal, int MODE = 0>
-__global__ void __launch_bounds__(k2_threads<LOGN1>(), 1) k2_column(Params prm) {
+__global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
     const int col = blockIdx.x;
     const int kp = col >> prm.log_n2;

@@ -75,6 +75,9 @@ HK_DEV void cp_async8(void *smem, const void *gmem) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 HK_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+HK_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>  // wait until at most N committed groups are still in flight
+HK_DEV void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Butterfly with twiddle omega^0 = 1 (GS and CT coincide): no multiplication.
 HK_DEV void bfly1(uint32_t &u, uint32_t &v, uint32_t p) {

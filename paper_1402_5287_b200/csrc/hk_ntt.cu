@@ -6,9 +6,8 @@
 //                        a and x tiles in one launch
 //   K2 k2_column         A2 matrix-index forward NTTs (N1) of X^ and A^ columns, A3 pointwise
 //                        Montgomery product, inverse matrix-index NTT, keep the n needed rows
-//   K3a k3a_row_intt     A3 inverse slice-dimension NTT per output row
-//   K3b k3b_carry    A3 Garner CRT -> signed coefficients, A4 carry propagation and
-//                        sign-magnitude output
+//   K3 k3_finish         A3 inverse slice-dimension NTT, Garner CRT -> signed coefficients,
+//                        A4 carry propagation and sign-magnitude output (one launch, rows tiled)
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -94,7 +93,6 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
     static_assert(LOGN2 >= 5 && TPR >= S1, "K1 tiling");
     extern __shared__ uint32_t sm[];
     __shared__ int8_t s_sign[kK1Rows];
-    __shared__ int s_nz[kK1Rows];
 
     const int tid = threadIdx.x;
     if (prm.hdr->magic != kWsMagic || prm.hdr->hash != prm.hash) {
@@ -127,33 +125,32 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
         for (int64_t c = tid; c < bytes / 16; c += T) cp_async16(d + 16 * c, g + 16 * c);
         if ((bytes & 15) && tid == 0) cp_async8(d + (bytes & ~int64_t(15)), g + (bytes & ~int64_t(15)));
         cp_async_wait_all();
+        __syncthreads();
     }
-    // ---- validation (A1): bits >= P zero, sign in {-1,0,1}, sign == 0 <=> magnitude == 0
-    const int rem = prm.P - 64 * (L - 1);
-    const uint64_t topmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
-    if (tid < kK1Rows) s_nz[tid] = 0;
-    __syncthreads();
-    bool bad = false;
-    for (int idx = tid; idx < kK1Rows * L; idx += T) {
-        const int r = idx / L, u = idx - (idx / L) * L;
-        const int64_t row = r0 + r;
-        if (row >= count) continue;
-        const uint64_t v = slimb[idx];
-        if (v) s_nz[r] = 1;
-        if (u == L - 1 && (v & ~topmask)) bad = true;
-    }
-    __syncthreads();
-    if (tid < kK1Rows) {
-        const int64_t row = r0 + tid;
-        int sg = 0;
-        if (row < count) {
-            sg = sgn[row];
-            if (sg < -1 || sg > 1 || ((sg == 0) != (s_nz[tid] == 0))) bad = true;
+    // ---- validation (A1): bits >= P zero, sign in {-1,0,1}, sign == 0 <=> magnitude == 0;
+    // one warp per row (no division by L, one vote per row)
+    {
+        const int rem = prm.P - 64 * (L - 1);
+        const uint64_t topmask = rem >= 64 ? ~0ull : ((1ull << rem) - 1);
+        const int lane = tid & 31;
+        for (int r = tid >> 5; r < kK1Rows; r += T / 32) {
+            const int64_t row = r0 + r;
+            int sg = 0;
+            if (row < count) {
+                const uint64_t *rp = slimb + r * L;
+                uint64_t orv = 0;
+                for (int u = lane; u < L; u += 32) orv |= rp[u];
+                const bool nz = __any_sync(0xffffffffu, orv != 0);
+                if (lane == 0) {
+                    sg = sgn[row];
+                    if ((rp[L - 1] & ~topmask) || sg < -1 || sg > 1 || ((sg == 0) == nz))
+                        atomicMin(&prm.hdr->status, (int)HK_ERANGE);
+                }
+            }
+            if (lane == 0) s_sign[r] = (int8_t)sg;
         }
-        s_sign[tid] = (int8_t)sg;
+        __syncthreads();
     }
-    if (bad) atomicMin(&prm.hdr->status, (int)HK_ERANGE);
-    __syncthreads();
 
     // ---- A1: this thread's digits t = j0 + m S1 (m < 16), extracted once for all primes
     const int r = tid / TPR, j0 = tid % TPR;
@@ -177,17 +174,24 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
         dhi[m] = (uint32_t)(lo >> 32);
     }
 
+    // N2 twiddle tables -> smem, double-buffered in the (now free) limb staging area: the table
+    // of prime kp + 2 streams in by cp.async while prime kp is transformed
+    auto fetch_tw = [&](int kp) {
+        uint4 *dst = reinterpret_cast<uint4 *>(slimb) + (kp & 1) * (N2 / 2);
+        const uint4 *src = reinterpret_cast<const uint4 *>(prm.tw + (size_t)kp * (prm.N2 + prm.N1));
+        for (int i = tid; i < N2 / 2; i += T) cp_async16(dst + i, src + i);
+        cp_async_commit();
+    };
+    __syncthreads();  // every thread is done with the limbs
+    fetch_tw(0);
+    fetch_tw(1);
     for (int kp = 0; kp < kNumPrimes; ++kp) {
         const uint32_t p = prm.pc[kp].p;
         const uint32_t *F = is_x ? prm.pc[kp].fx : prm.pc[kp].fa;
         const uint32_t *Fq = is_x ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
-        // this prime's N2 twiddle table -> smem (the limb staging area is free after extraction)
-        uint2 *tw = reinterpret_cast<uint2 *>(slimb);
-        __syncthreads();
-        {
-            const uint4 *src = reinterpret_cast<const uint4 *>(prm.tw + (size_t)kp * (prm.N2 + prm.N1));
-            for (int i = tid; i < N2 / 2; i += T) reinterpret_cast<uint4 *>(tw)[i] = src[i];
-        }
+        const uint2 *tw = reinterpret_cast<const uint2 *>(slimb) + (kp & 1) * N2;
+        if (kp + 1 < kNumPrimes) cp_async_wait_group<1>();
+        else cp_async_wait_group<0>();
         __syncthreads();
         if (act) {
             uint32_t v[G1];
@@ -244,17 +248,31 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
             }
         }
         __syncthreads();
+        if (kp + 2 < kNumPrimes) fetch_tw(kp + 2);
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// K3a: for a tile of k3_rows() output rows and all 5 primes: inverse slice-dimension NTT (DIT with
-// forward roots, slice index negated), then Garner CRT (balanced mixed radix) of every
-// coefficient C_s, |C_s| < M/2 < 2^155, written as five 32-bit two's-complement words
-// Ycoef[(row * 5 + word) * ldS + s] (word planes: coalesced stores here and loads in K3b).
+// K3 (fused): for R = k3_rows() output rows and all 5 primes in shared memory
+//   (a) inverse slice-dimension NTT (DIT with forward roots: slice index negated),
+//   (b) Garner CRT of every coefficient C_s, |C_s| < M/2 < 2^155, as five 32-bit
+//       two's-complement words written in place over the residues,
+//   (c) per row: Y = sum_s C_s 2^(w s) mod 2^(64 Ly) gathered limb by limb (w in {64, 65}
+//       makes the limb index q(s) = floor(w s / 64) injective), carries resolved by a block
+//       scan of carry-transfer functions, two's complement -> sign-magnitude, coalesced store.
+// Shared layout: word (prime kp, slice sigma, row r) at kp * N2 * R + swz(sigma) * R + r with
+// swz(sigma) = sigma ^ ((sigma >> 5) & (32/R - 1)): rows interleaved so one 16-byte cp.async
+// brings the R rows of a (prime, sigma) column segment; the XOR keeps the strided (S >= 32/R)
+// and the contiguous (S = 1, radix 32) passes and the Garner pairs bank-conflict-free.
 template <int LOGN2>
-constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : 4; }  // 5 x rows x N2 words in smem
-constexpr int kK3aThreads = 320;  // 5 primes x 4 rows x 32 groups = 2 groups per thread
+constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : 4; }
+
+template <int LOGN2>
+struct K3Layout {
+    static constexpr int N2 = 1 << LOGN2, R = k3_rows<LOGN2>(), OCT = 32 / R, PS = N2 * R;
+    static HK_DEV int idx(int kp, int s, int r) { return kp * PS + (s ^ ((s >> 5) & (OCT - 1))) * R + r; }
+    static constexpr size_t res_words() { return (size_t)kNumPrimes * PS; }
+};
 
 // Garner CRT with standard mixed-radix digits u_k in [0, p_k):
 //   C' = u0 + p0 (u1 + p1 (u2 + p2 (u3 + p3 u4)))  in [0, M),  M = p0 p1 p2 p3 p4 < 2^155,
@@ -308,24 +326,25 @@ HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint32_t (&c
     cw[0] = a0; cw[1] = a1; cw[2] = a2; cw[3] = a3; cw[4] = a4;
 }
 
-template <int LOGN2, int R, int S>
-HK_DEV void k3_dit_pass_all(uint32_t *sm, const Params &prm) {
-    constexpr int N = 1 << LOGN2, G = 1 << R, NG = N / G;
-    constexpr int RS = k1_row_stride<LOGN2>();
-    constexpr int total = kNumPrimes * k3_rows<LOGN2>() * NG;
-    for (int gi = threadIdx.x; gi < total; gi += kK3aThreads) {
-        const int b = gi / NG, g = gi % NG;  // b = kp * k3_rows<LOGN2>() + row
-        const int kp = b / k3_rows<LOGN2>();
+constexpr int kK3Block = 320;  // 5 primes x 4 rows x 32 groups = 2 radix-32 groups per thread
+
+// Inverse DIT pass of radix 2^RR at stride S over all (prime, row) transforms of the tile.
+template <int LOGN2, int RR, int S>
+HK_DEV void k3_dit_pass(uint32_t *sm, const Params &prm) {
+    using LY = K3Layout<LOGN2>;
+    constexpr int N = 1 << LOGN2, G = 1 << RR, NG = N / G, R = LY::R;
+    constexpr int total = kNumPrimes * R * NG;
+    for (int gi = threadIdx.x; gi < total; gi += kK3Block) {
+        const int r = gi % R, rest = gi / R;
+        const int g = rest % NG, kp = rest / NG;
         const uint32_t p = prm.pc[kp].p;
         const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
-        const int j0 = g % S;
-        const int B = (g / S) * (S * G);
-        uint32_t *base = sm + b * RS;
+        const int j0 = g % S, B = (g / S) * (S * G);
         uint32_t v[G];
 #pragma unroll
-        for (int m = 0; m < G; ++m) v[m] = base[pad(B + j0 + m * S)];
+        for (int m = 0; m < G; ++m) v[m] = sm[LY::idx(kp, B + j0 + m * S, r)];
 #pragma unroll
-        for (int l = 0; l < R; ++l) {
+        for (int l = 0; l < RR; ++l) {
             const int half = 1 << l;
 #pragma unroll
             for (int m = 0; m < G; ++m) {
@@ -335,60 +354,21 @@ HK_DEV void k3_dit_pass_all(uint32_t *sm, const Params &prm) {
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) base[pad(B + j0 + m * S)] = v[m];
+        for (int m = 0; m < G; ++m) sm[LY::idx(kp, B + j0 + m * S, r)] = v[m];
     }
     __syncthreads();
 }
 template <int LOGN2, int LO>
-struct K3DitPasses {
+struct K3Dit {  // radix-32 bottom pass (S = 1) first, then passes of radix <= 32 at S >= 32
     static HK_DEV void run(uint32_t *sm, const Params &prm) {
         if constexpr (LO < LOGN2) {
-            constexpr int R = (LOGN2 - LO) < 5 ? (LOGN2 - LO) : 5;
-            k3_dit_pass_all<LOGN2, R, (1 << LO)>(sm, prm);
-            K3DitPasses<LOGN2, LO + R>::run(sm, prm);
+            constexpr int RR = (LOGN2 - LO) < 5 ? (LOGN2 - LO) : 5;
+            k3_dit_pass<LOGN2, RR, (1 << LO)>(sm, prm);
+            K3Dit<LOGN2, LO + RR>::run(sm, prm);
         }
     }
 };
 
-template <int LOGN2>
-__global__ void __launch_bounds__(kK3aThreads, 2) k3a_row_intt_crt(Params prm) {
-    constexpr int N2 = 1 << LOGN2;
-    constexpr int RS = k1_row_stride<LOGN2>();
-    extern __shared__ uint32_t sm[];  // [prime][row][RS]
-    const int tid = threadIdx.x;
-    const int64_t r0 = prm.row0 + (int64_t)blockIdx.x * k3_rows<LOGN2>();
-    const int64_t m = prm.m;
-    for (int idx = tid; idx < kNumPrimes * N2 * k3_rows<LOGN2>(); idx += kK3aThreads) {
-        const int r = idx % k3_rows<LOGN2>(), cs = idx / k3_rows<LOGN2>();  // cs = kp * N2 + sigma
-        const int64_t row = r0 + r;
-        const int kp = cs / N2, sigma = cs % N2;
-        uint32_t *dst = sm + (kp * k3_rows<LOGN2>() + r) * RS + pad(sigma);
-        if (row < m) cp_async4(dst, prm.Yhat + (int64_t)cs * prm.ldY + row);
-        else *dst = 0u;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-    K3DitPasses<LOGN2, 0>::run(sm, prm);
-    const int S2 = prm.S2;
-    for (int idx = tid; idx < k3_rows<LOGN2>() * S2; idx += kK3aThreads) {
-        const int r = idx / S2, t = idx - (idx / S2) * S2;
-        const int64_t row = r0 + r;
-        if (row >= m) continue;
-        uint32_t res[kNumPrimes];
-        const int pos = pad((N2 - t) & (N2 - 1));  // slice index negated (forward-root DIT)
-#pragma unroll
-        for (int kp = 0; kp < kNumPrimes; ++kp) res[kp] = sm[(kp * k3_rows<LOGN2>() + r) * RS + pos];
-        uint32_t cw[kNumPrimes];
-        garner(res, prm, cw);
-        uint32_t *dst = prm.Yres + row * kNumPrimes * prm.ldS + t;
-#pragma unroll
-        for (int k = 0; k < kNumPrimes; ++k) dst[k * prm.ldS] = cw[k];  // bit 159 = sign
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// K3b: Y = sum_s C_s 2^(w s) mod 2^(64 Ly), carry propagation by a block scan of
-// carry-transfer functions, two's complement -> sign-magnitude.
 // carry-transfer function {-1,0,1} -> {-1,0,1}, packed 2 bits per input (value + 1)
 HK_DEV int tf_apply(int f, int c) { return ((f >> (2 * (c + 1))) & 3) - 1; }
 HK_DEV int tf_compose(int g, int f) {  // g o f
@@ -399,86 +379,129 @@ HK_DEV int tf_compose(int g, int f) {  // g o f
 }
 constexpr int kTfId = (0) | (1 << 2) | (2 << 4);
 
-// One CTA per output row.  Coefficient s (160-bit two's complement C_s, w in {64, 65}) sits at
-// limb q(s) = floor(w s / 64), bit sh = w s mod 64; its shifted value C_s 2^sh spans the four
-// words S_0..S_3 (sign-extended to 256 bits) plus a -1 borrow into limb q + 4 when C_s < 0.
-// Because q is injective for w >= 64, word d of every coefficient lands in its own slot
-// P_d[q(s) + d]; limb l's sum is P_0[l] + P_1[l] + P_2[l] + P_3[l] - borrow[l].
-template <int CHUNK>  // limbs per thread = ceil(Ly / kK3Threads)
-__global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
-    extern __shared__ uint64_t sP[];  // [4][Ly] words, then borrow bytes [Ly]
-    __shared__ uint8_t s_ecarry[kK3Threads];
-    __shared__ int s_wtot[kK3Threads / 32];
-    __shared__ int s_wcarry[kK3Threads / 32];
-    __shared__ int s_neg, s_zmin;
+// coefficient index s with limb index q(s) = floor(w s / 64) == qq (w in {64, 65}), else -1;
+// *sh = w s mod 64.  w = 65: s = 64 a + b, q = 65 a + b (b < 64).
+HK_DEV int k3_coef_of_limb(int qq, int w, int *sh) {
+    if (w == 64) { *sh = 0; return qq; }
+    const int a = qq / 65, b = qq - 65 * a;
+    *sh = b;
+    return b < 64 ? 64 * a + b : -1;
+}
+
+template <int LOGN2, int CH>  // CH = limbs per thread = ceil(Ly / (kK3Block / R))
+__global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
+    using LY = K3Layout<LOGN2>;
+    constexpr int N2 = 1 << LOGN2, R = LY::R, T = kK3Block;
+    extern __shared__ uint32_t sm[];  // residues -> CRT words [5][N2][R] (swizzled) -> y rows [R][Ly]
+    __shared__ int s_wtot[T / 32 * R], s_wcarry[T / 32 * R];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t row = prm.row0 + blockIdx.x;
-    const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
-    uint8_t *sB = reinterpret_cast<uint8_t *>(sP + 4 * Ly);
-    {  // zero the slot arrays (positions without a coefficient stay 0)
-        uint4 *z = reinterpret_cast<uint4 *>(sP);
-        const int n16 = (4 * Ly * 8 + Ly + 15) / 16;
-        for (int i = tid; i < n16; i += kK3Threads) z[i] = make_uint4(0, 0, 0, 0);
-    }
-    if (tid == 0) { s_neg = 0; s_zmin = INT_MAX; }
-    __syncthreads();
-    const uint32_t *src = prm.Yres + row * kNumPrimes * prm.ldS;
-    const int64_t ldS = prm.ldS;
-    for (int s = tid; s < S2; s += kK3Threads) {
-        const uint32_t w0 = __ldcs(src + s), w1 = __ldcs(src + ldS + s), w2 = __ldcs(src + 2 * ldS + s),
-                       w3 = __ldcs(src + 3 * ldS + s), w4 = __ldcs(src + 4 * ldS + s);
-        const uint64_t C0 = (uint64_t)w0 | ((uint64_t)w1 << 32);
-        const uint64_t C1 = (uint64_t)w2 | ((uint64_t)w3 << 32);
-        const uint64_t C2 = (uint64_t)(int64_t)(int32_t)w4;  // sign-extend bit 159
-        const uint64_t C3 = (uint64_t)((int64_t)C2 >> 63);
-        const int o = w * s, q = o >> 6, sh = o & 63;
-        uint64_t S0 = C0, S1 = C1, S2w = C2, S3 = C3;
-        if (sh) {
-            S3 = (C3 << sh) | (C2 >> (64 - sh));
-            S2w = (C2 << sh) | (C1 >> (64 - sh));
-            S1 = (C1 << sh) | (C0 >> (64 - sh));
-            S0 = C0 << sh;
+    const int64_t r0 = prm.row0 + (int64_t)blockIdx.x * R;
+    const int64_t m = prm.m;
+
+    // (0) Y^ columns of the R rows, all primes -> smem
+    {
+        const bool vec = r0 + R <= m && ((r0 & (R - 1)) == 0);
+        for (int e = tid; e < kNumPrimes * N2; e += T) {
+            const int kp = e >> LOGN2, sg = e & (N2 - 1);
+            const uint32_t *g = prm.Yhat + (int64_t)(kp * N2 + sg) * prm.ldY + r0;
+            uint32_t *d = sm + LY::idx(kp, sg, 0);
+            if (vec) {
+                if constexpr (R == 4) cp_async16(d, g);
+                else cp_async8(d, g);
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) d[r] = r0 + r < m ? g[r] : 0u;
+            }
         }
-        if (q < Ly) sP[q] = S0;
-        if (q + 1 < Ly) sP[Ly + q + 1] = S1;
-        if (q + 2 < Ly) sP[2 * Ly + q + 2] = S2w;
-        if (q + 3 < Ly) sP[3 * Ly + q + 3] = S3;
-        if (C3 && q + 4 < Ly) sB[q + 4] = 1;
+        cp_async_wait_all();
+        __syncthreads();
+    }
+    // (a) inverse slice NTTs
+    K3Dit<LOGN2, 0>::run(sm, prm);
+    // (b) Garner CRT in place: coefficient s lives at sigma = (N2 - s) mod N2 and its CRT words
+    // go to sigma = s, so the pair {s, N2 - s} is read and written by one thread.
+    for (int it = tid; it < R * (N2 / 2 + 1); it += T) {
+        const int r = it % R, s1 = it / R, s2 = (N2 - s1) & (N2 - 1);
+        uint32_t ra[kNumPrimes], rb[kNumPrimes], ca[kNumPrimes], cb[kNumPrimes];
+#pragma unroll
+        for (int kp = 0; kp < kNumPrimes; ++kp) {
+            ra[kp] = sm[LY::idx(kp, s2, r)];
+            rb[kp] = sm[LY::idx(kp, s1, r)];
+        }
+        garner(ra, prm, ca);
+#pragma unroll
+        for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, s1, r)] = ca[k];
+        if (s2 != s1) {
+            garner(rb, prm, cb);
+#pragma unroll
+            for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, s2, r)] = cb[k];
+        }
     }
     __syncthreads();
 
-    const int l0 = tid * CHUNK;
-    uint64_t u[CHUNK];
-    int e[CHUNK];
+    // (c) all R rows at once: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R),
+    // so the R rows' words of a coefficient are read by adjacent lanes.
+    const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
+    const int r = tid % R, k = tid / R, lane_r = lane / R;  // lane_r: position among the row's lanes
+    const int64_t row = r0 + r;
+    const int l0 = k * CH;
+    uint64_t u[CH];
+    int e[CH];
 #pragma unroll
-    for (int c = 0; c < CHUNK; ++c) {
+    for (int c = 0; c < CH; ++c) {
         const int l = l0 + c;
         uint64_t acc = 0;
         int hi = 0;
         if (l < Ly) {
-            acc = sP[l];
-            uint64_t t = sP[Ly + l];
-            acc += t; hi += acc < t;
-            t = sP[2 * Ly + l];
-            acc += t; hi += acc < t;
-            t = sP[3 * Ly + l];
-            acc += t; hi += acc < t;
-            const int bw = sB[l];
-            hi -= bw & (acc == 0);
-            acc -= bw;
+#pragma unroll
+            for (int d = 0; d < 5; ++d) {  // word d of coefficient s with q(s) = l - d; d = 4: sign borrow
+                const int qq = l - d;
+                if (qq < 0) break;
+                int sh;
+                const int s = k3_coef_of_limb(qq, w, &sh);
+                if (s < 0 || s >= S2) continue;
+                const uint32_t w4 = sm[LY::idx(4, s, r)];
+                const uint64_t C3 = (uint64_t)((int64_t)(int32_t)w4 >> 31);  // sign word
+                if (d == 4) {  // -1 at limb q + 4 when C_s < 0 (sign extension beyond S_3)
+                    const uint64_t bw = C3 & 1u;
+                    hi -= (int)(bw & (acc == 0));
+                    acc -= bw;
+                    continue;
+                }
+                const uint64_t C2 = (uint64_t)(int64_t)(int32_t)w4;
+                uint64_t cd, cm;  // C_d and C_{d-1}
+                if (d == 0) {
+                    cd = (uint64_t)sm[LY::idx(0, s, r)] | ((uint64_t)sm[LY::idx(1, s, r)] << 32);
+                    cm = 0;
+                } else if (d == 1) {
+                    cd = (uint64_t)sm[LY::idx(2, s, r)] | ((uint64_t)sm[LY::idx(3, s, r)] << 32);
+                    cm = (uint64_t)sm[LY::idx(0, s, r)] | ((uint64_t)sm[LY::idx(1, s, r)] << 32);
+                } else if (d == 2) {
+                    cd = C2;
+                    cm = (uint64_t)sm[LY::idx(2, s, r)] | ((uint64_t)sm[LY::idx(3, s, r)] << 32);
+                } else {
+                    cd = C3;
+                    cm = C2;
+                }
+                const uint64_t word = sh ? ((cd << sh) | (cm >> (64 - sh))) : cd;
+                acc += word;
+                hi += acc < word;
+            }
         }
         u[c] = acc;
-        e[c] = hi;  // carry into limb l+1, in [-1, 3]
+        e[c] = hi;  // carry into limb l + 1, in [-1, 3]
     }
-    s_ecarry[tid] = (uint8_t)(e[CHUNK - 1] + 1);
+    // the carry out of the previous chunk of the same row (thread t - R) comes via smem
+    __shared__ int8_t s_ecarry[T];
+    __shared__ int s_neg[R], s_zmin[R];
+    s_ecarry[tid] = (int8_t)e[CH - 1];
+    if (tid < R) { s_neg[tid] = 0; s_zmin[tid] = INT_MAX; }
     __syncthreads();
-    // u_l = w_l + e_{l-1} -> g_l in {-1,0,1}; transfer f_l(c) = g_l + [c=1, u_l=MAX] - [c=-1, u_l=0]
-    // packed 2 bits per input c in {-1,0,1}: (f(-1)+1) | (f(0)+1) << 2 | (f(1)+1) << 4
     int F = kTfId;
-    int fl[CHUNK];
-    int ein = tid > 0 ? (int)s_ecarry[tid - 1] - 1 : 0;
+    int fl[CH];
+    int ein = k > 0 ? (int)s_ecarry[tid - R] : 0;
 #pragma unroll
-    for (int c = 0; c < CHUNK; ++c) {
+    for (int c = 0; c < CH; ++c) {
         const uint64_t wv = u[c];
         const uint64_t uv = wv + (uint64_t)(int64_t)ein;
         const int g = (ein > 0 && uv < wv) ? 1 : ((ein < 0 && uv > wv) ? -1 : 0);
@@ -489,51 +512,62 @@ __global__ void __launch_bounds__(kK3Threads) k3b_carry(Params prm) {
         F = tf_compose(f, F);
         ein = e[c];
     }
-    // block scan of transfer functions (low limbs first)
+    // segmented scan of transfer functions over the chunks of each row (lanes r, r + R, ...)
     int incl = F;
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
+    for (int off = R; off < 32; off <<= 1) {
         const int other = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl = tf_compose(incl, other);
     }
-    if (lane == 31) s_wtot[warp] = incl;
+    if (lane >= 32 - R) s_wtot[warp * R + (lane - (32 - R))] = incl;  // per (warp, row) total
     __syncthreads();
-    if (tid == 0) {
+    if (tid < R) {  // carry into each warp's first chunk of row tid
         int c = 0;
-        for (int wi = 0; wi < kK3Threads / 32; ++wi) {
-            s_wcarry[wi] = c;
-            c = tf_apply(s_wtot[wi], c);
+        for (int wi = 0; wi < T / 32; ++wi) {
+            s_wcarry[wi * R + tid] = c;
+            c = tf_apply(s_wtot[wi * R + tid], c);
         }
     }
     __syncthreads();
-    const int prev = __shfl_up_sync(0xffffffffu, incl, 1);
-    int carry = s_wcarry[warp];
-    if (lane > 0) carry = tf_apply(prev, carry);
+    const int prev = __shfl_up_sync(0xffffffffu, incl, R);
+    int carry = s_wcarry[warp * R + r];
+    if (lane_r > 0) carry = tf_apply(prev, carry);
     int zloc = INT_MAX;
 #pragma unroll
-    for (int c = 0; c < CHUNK; ++c) {  // final limbs (mod 2^(64 Ly))
+    for (int c = 0; c < CH; ++c) {  // final limbs (mod 2^(64 Ly))
         const uint64_t v = u[c] + (uint64_t)(int64_t)carry;
         carry = tf_apply(fl[c], carry);
         u[c] = v;
         if (l0 + c < Ly && v && zloc == INT_MAX) zloc = l0 + c;
-        if (l0 + c == Ly - 1) s_neg = (int)(v >> 63);
+        if (l0 + c == Ly - 1) s_neg[r] = (int)(v >> 63);
     }
-    if (zloc != INT_MAX) atomicMin(&s_zmin, zloc);
-    __syncthreads();
-    const bool neg = s_neg != 0;
-    const int zmin = s_zmin;
-    const int64_t orow = prm.reverse_out ? (prm.m - 1 - row) : row;
-    uint64_t *yo = prm.y_mag + orow * Ly;
+    if (zloc != INT_MAX) atomicMin(&s_zmin[r], zloc);
+    __syncthreads();  // also: every CRT word has been read, the residue area is free
+    uint64_t *ybuf = reinterpret_cast<uint64_t *>(sm);  // [R][Ly]
+    {
+        const bool neg = s_neg[r] != 0;
+        const int zmin = s_zmin[r];
 #pragma unroll
-    for (int c = 0; c < CHUNK; ++c) {
-        const int l = l0 + c;
-        if (l < Ly) {
-            uint64_t v = u[c];
-            if (neg) v = l < zmin ? 0ull : (l == zmin ? (0ull - v) : ~v);
-            yo[l] = v;
+        for (int c = 0; c < CH; ++c) {
+            const int l = l0 + c;
+            if (l < Ly) {
+                uint64_t v = u[c];
+                if (neg) v = l < zmin ? 0ull : (l == zmin ? (0ull - v) : ~v);
+                ybuf[r * Ly + l] = v;
+            }
         }
     }
-    if (tid == 0) prm.y_sign[orow] = neg ? (int8_t)-1 : (zmin < Ly ? (int8_t)1 : (int8_t)0);
+    __syncthreads();
+    for (int rr = 0; rr < R; ++rr) {
+        const int64_t orow_r = r0 + rr;
+        if (orow_r >= m) break;
+        const int64_t orow = prm.reverse_out ? (m - 1 - orow_r) : orow_r;
+        uint64_t *yo = prm.y_mag + orow * Ly;
+        for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
+        if (tid == 0)
+            prm.y_sign[orow] = s_neg[rr] ? (int8_t)-1 : (s_zmin[rr] < Ly ? (int8_t)1 : (int8_t)0);
+    }
+    (void)row;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -566,30 +600,13 @@ static int launch_rows(const Params &prm0, cudaStream_t st, int tile0 = 0, int n
     Params prm = prm0;
     prm.tile0 = tile0;
     const size_t limb_bytes = (size_t)kK1Rows * prm.L * sizeof(uint64_t);
-    const size_t tab_bytes = (size_t)(1 << LOGN2) * sizeof(uint2);  // reuses the limb area
+    const size_t tab_bytes = (size_t)2 * (1 << LOGN2) * sizeof(uint2);  // 2 tables, reuse the limb area
     const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t) +
                          (limb_bytes > tab_bytes ? limb_bytes : tab_bytes);
     if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess)
         return HK_ECUDA;
     k1_slice_rowntt<LOGN2><<<ntiles, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
-    return check_launch();
-}
-
-template <int LOGN2>
-static int launch_rows_inverse(const Params &prm0, cudaStream_t st, int64_t row0 = 0,
-                               int64_t nrows = -1) {
-    if (nrows < 0) nrows = prm0.m - row0;
-    if (nrows <= 0) return HK_OK;
-    Params prm = prm0;
-    prm.row0 = row0;
-    const size_t smem =
-        (size_t)kNumPrimes * k3_rows<LOGN2>() * k1_row_stride<LOGN2>() * sizeof(uint32_t);
-    if (cudaFuncSetAttribute(k3a_row_intt_crt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return HK_ECUDA;
-    const unsigned grid = (unsigned)((nrows + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
-    k3a_row_intt_crt<LOGN2><<<grid, kK3aThreads, smem, st>>>(prm);
     return check_launch();
 }
 
@@ -679,36 +696,42 @@ int launch_k1_range(const Params &prm, void *stream, int tile0, int ntiles) {
     }
 }
 
+template <int LOGN2, int CH>
+static int launch_k3(const Params &prm, cudaStream_t st, int64_t nrows) {
+    const size_t ybytes = (size_t)k3_rows<LOGN2>() * prm.Ly * sizeof(uint64_t);  // y rows reuse the area
+    const size_t rbytes = K3Layout<LOGN2>::res_words() * sizeof(uint32_t);
+    const size_t smem = rbytes > ybytes ? rbytes : ybytes;
+    if (cudaFuncSetAttribute(k3_finish<LOGN2, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    const unsigned grid = (unsigned)((nrows + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
+    k3_finish<LOGN2, CH><<<grid, kK3Block, smem, st>>>(prm);
+    return check_launch();
+}
+
+template <int LOGN2>
+static int launch_k3_ch(const Params &prm, cudaStream_t st, int64_t nrows) {
+    constexpr int TR = kK3Block / k3_rows<LOGN2>();  // threads per row
+    switch ((prm.Ly + TR - 1) / TR) {
+#define HK_CASE(C) case C: return launch_k3<LOGN2, C>(prm, st, nrows);
+        HK_CASE(1) HK_CASE(2) HK_CASE(3) HK_CASE(4) HK_CASE(5) HK_CASE(6) HK_CASE(7)
+        HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12) HK_CASE(13) HK_CASE(14)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
+}
+
 int launch_k3_range(const Params &prm0, void *stream, int64_t row0, int64_t nrows) {
+    if (nrows <= 0) return HK_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    int rc = HK_OK;
-    switch (prm0.log_n2) {
-#define HK_CASE(LG) case LG: rc = launch_rows_inverse<LG>(prm0, st, row0, nrows); break;
+    Params prm = prm0;
+    prm.row0 = row0;
+    switch (prm.log_n2) {
+#define HK_CASE(LG) case LG: return launch_k3_ch<LG>(prm, st, nrows);
         HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11)
 #undef HK_CASE
         default: return HK_EUNSUPPORTED;
     }
-    if (rc) return rc;
-    if (nrows <= 0) return HK_OK;
-    Params prm = prm0;
-    prm.row0 = row0;
-    const size_t smem3 = ((size_t)4 * prm.Ly * 8 + prm.Ly + 15) / 16 * 16;
-    const int chunk = (prm.Ly + kK3Threads - 1) / kK3Threads;
-    switch (chunk) {
-#define HK_CASE(C)                                                                             \
-    case C:                                                                                    \
-        if (cudaFuncSetAttribute(k3b_carry<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                                 (int)smem3) != cudaSuccess)                                   \
-            return HK_ECUDA;                                                                   \
-        k3b_carry<C><<<(unsigned)nrows, kK3Threads, smem3, st>>>(prm);                         \
-        break;
-        HK_CASE(1) HK_CASE(2) HK_CASE(3) HK_CASE(4) HK_CASE(5) HK_CASE(6) HK_CASE(7) HK_CASE(8)
-        HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12) HK_CASE(13) HK_CASE(14) HK_CASE(15)
-        HK_CASE(16) HK_CASE(17)
-#undef HK_CASE
-        default: return HK_EUNSUPPORTED;
-    }
-    return check_launch();
 }
 
 }  // namespace hk

@@ -51,7 +51,6 @@ struct Params {
     int64_t out_off;             // first needed index of the matrix-index convolution
     int64_t ldA, ldX, ldY, ldS;  // leading dims (elements) of the transform-domain arrays
     uint64_t hash;
-    int32_t diag;                // diagnostics-only switches (HK_K2_DIAG); 0 in production
     int32_t tile0;               // K1: first tile of this launch (combined [a tiles | x tiles] index)
     int64_t row0;                // K3: first output row of this launch
     // inputs / outputs (device)

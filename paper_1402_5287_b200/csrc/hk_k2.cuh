@@ -325,7 +325,6 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
 
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
 // MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT).
-// TW = TwConst is a diagnostics-only variant (HK_K2_DIAG=1; wrong results).
 template <int LOGN1, class TW = TwGlobal, int MODE = 0>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];

@@ -90,9 +90,6 @@ HK_DEV void bfly1(uint32_t &u, uint32_t &v, uint32_t p) {
 struct TwGlobal {
     static HK_DEV uint2 ld(const uint2 *t, int i) { return __ldg(t + i); }
 };
-struct TwConst {  // diagnostics only: a fixed twiddle (wrong results), measures twiddle-load cost
-    static HK_DEV uint2 ld(const uint2 *t, int i) { return make_uint2(1234567u + (i & 1), 2468u); }
-};
 struct TwShared {
     static HK_DEV uint2 ld(const uint2 *t, int i) { return t[i]; }
 };

@@ -617,22 +617,7 @@ static int launch_cols(const Params &prm, cudaStream_t st) {
     if (cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
-    // one CTA per SM: keep the carveout minimal so the N1 twiddle table stays L1-resident
-    const int pct = (int)((smem + 2048) * 100 / (228 * 1024)) + 1;
-    if (getenv("HK_K2_CARVEOUT"))
-        cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             atoi(getenv("HK_K2_CARVEOUT")));
-    (void)pct;
-    const int diag = getenv("HK_K2_DIAG") ? atoi(getenv("HK_K2_DIAG")) : 0;  // diagnostics only
-    Params p2 = prm;
-    p2.diag = diag;
-    if (diag & 1) {
-        cudaFuncSetAttribute(k2_column<LOGN1, TwConst>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        k2_column<LOGN1, TwConst><<<ncols, k2_threads<LOGN1>(), smem, st>>>(p2);
-    } else {
-        k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(p2);
-    }
+    k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
 }
 

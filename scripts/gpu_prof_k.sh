@@ -9,5 +9,7 @@ for KRE in $KRES; do
   python scripts/ncu_summary.py /tmp/prof_$KRE.ncu-rep gpurun_out/prof_$KRE.json > /dev/null
   python scripts/ncu_lines.py /tmp/prof_$KRE.ncu-rep "$KRE" 45 > gpurun_out/lines_$KRE.txt
   python scripts/ncu_opcodes.py /tmp/prof_$KRE.ncu-rep "$KRE" > gpurun_out/opcodes_$KRE.txt
-  [ "$KEEP" = 1 ] && cp /tmp/prof_$KRE.ncu-rep gpurun_out/
+  [ -n "$PHASES" ] && python scripts/ncu_phases.py /tmp/prof_$KRE.ncu-rep "$KRE" $PHASES > gpurun_out/phases_$KRE.txt
+  if [ "$KEEP" = 1 ]; then cp /tmp/prof_$KRE.ncu-rep gpurun_out/; fi
 done
+true

@@ -164,6 +164,21 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P,
                        uint64_t *y_mag_host, int8_t *y_sign_host,
                        void *ws, size_t ws_bytes, void *stream);
 
+/* Asynchronous end-to-end call with HOST buffers, for throughput over a stream of independent
+ * problems: enqueues on `stream`, in stream order and without synchronising, the H2D copies of a
+ * and x into ws's staging area, the matvec, the D2H copies of y and of the call's data status
+ * (one int32 hk_status written to *status_host when the stream reaches it).  Returns after
+ * enqueueing: argument errors synchronously, HK_OK otherwise; host buffers must stay valid (and
+ * y / status unread) until the stream has passed the call.  Several calls may be in flight on
+ * different streams with DIFFERENT workspaces; their copies then overlap each other's kernels
+ * (PCIe is full duplex).  Host buffers must be pinned for the copies to be asynchronous; ws as
+ * for hk_matvec_host (HK_WS_STAGING). */
+int32_t hk_matvec_host_async(int32_t kind, int64_t m, int64_t n, int32_t P,
+                             const uint64_t *a_mag_host, const int8_t *a_sign_host,
+                             const uint64_t *x_mag_host, const int8_t *x_sign_host,
+                             uint64_t *y_mag_host, int8_t *y_sign_host, int32_t *status_host,
+                             void *ws, size_t ws_bytes, void *stream);
+
 /* Pipeline stages of the NTT path, for per-kernel timing (bench.py) and phase-wise use:
  *   HK_STAGE_SLICE_ROWS  K1: validation, slicing, slice-dimension forward NTT of a and x
  *   HK_STAGE_COLUMNS     K2: matrix-index forward NTTs, pointwise product, inverse NTT

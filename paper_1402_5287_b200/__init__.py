@@ -67,6 +67,7 @@ def _load():
         "hk_circulant_matvec": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_hankel_rect_matvec": (i32, [i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_host": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_matvec_host_async": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_schoolbook_matvec": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
         "hk_matvec_stages": (i32, [i32, i64, i64, i32, ctypes.c_uint32, vp, vp, vp, vp, vp, vp,
                                    vp, sz, vp]),
@@ -85,7 +86,7 @@ def _load():
 _lib = _load()
 EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_workspace_size",
             "hk_workspace_init", "hk_workspace_status", "hk_hankel_matvec", "hk_toeplitz_matvec",
-            "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host",
+            "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host", "hk_matvec_host_async",
             "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
             "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
@@ -254,6 +255,65 @@ def matvec_host(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None
                              hptr(out[0]), hptr(out[1]), ws.ptr, ws.nbytes, _stream_ptr(stream))
     _check(rc, "hk_matvec_host")
     return out
+
+
+class HostPipeline:
+    """Throughput over a stream of independent problems with HOST buffers (hk_matvec_host_async):
+    ``depth`` lanes, each a CUDA stream with its own staging workspace; submit() enqueues a whole
+    call (H2D of a and x, the matvec, D2H of y and of the data status) on the next lane, so one
+    call's copies overlap other calls' kernels.  Host buffers should be pinned.  A lane is reused
+    only after its previous call has completed (submit() waits for it)."""
+
+    def __init__(self, kind, n, P, m=None, depth=3, device=None):
+        import torch
+        self.kind, self.n, self.P = int(kind), int(n), int(P)
+        self.m = self.n if m is None else int(m)
+        self.depth = int(depth)
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(self.depth)]
+        self.ws = []
+        for st in self.streams:
+            self.ws.append(Workspace(kind, self.n, P, m=self.m, flags=WS_STAGING, stream=st))
+        self.status = torch.zeros((self.depth,), dtype=torch.int32).pin_memory()
+        self.events = [None] * self.depth
+        self.k = 0
+        torch.cuda.synchronize(dev)
+
+    def submit(self, a_mag, a_sign, x_mag, x_sign, out):
+        """Enqueue one call; out = (y_mag, y_sign) pinned host tensors.  Returns the lane index."""
+        import torch
+        lane = self.k % self.depth
+        self.k += 1
+        if self.events[lane] is not None:
+            self.events[lane].synchronize()
+            self._check_lane(lane)
+        st, ws = self.streams[lane], self.ws[lane]
+
+        def hptr(a):
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+
+        rc = _lib.hk_matvec_host_async(self.kind, self.m, self.n, self.P, hptr(a_mag), hptr(a_sign),
+                                       hptr(x_mag), hptr(x_sign), hptr(out[0]), hptr(out[1]),
+                                       self.status.data_ptr() + 4 * lane, ws.ptr, ws.nbytes,
+                                       st.cuda_stream)
+        _check(rc, "hk_matvec_host_async")
+        ev = torch.cuda.Event()
+        ev.record(st)
+        self.events[lane] = ev
+        return lane
+
+    def _check_lane(self, lane):
+        code = int(self.status[lane].item())
+        if code != HK_OK:
+            raise HKError(code, "hk_matvec_host_async data status")
+
+    def drain(self):
+        """Wait for every call in flight and check their data status."""
+        for lane, ev in enumerate(self.events):
+            if ev is not None:
+                ev.synchronize()
+                self._check_lane(lane)
+                self.events[lane] = None
 
 
 class Problem:

@@ -485,6 +485,45 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
     return ds;
 }
 
+int32_t hk_matvec_host_async(int32_t kind, int64_t m, int64_t n, int32_t P,
+                             const uint64_t *a_mag_host, const int8_t *a_sign_host,
+                             const uint64_t *x_mag_host, const int8_t *x_sign_host,
+                             uint64_t *y_mag_host, int8_t *y_sign_host, int32_t *status_host,
+                             void *ws, size_t ws_bytes, void *stream) {
+    if (!a_mag_host || !a_sign_host || !x_mag_host || !x_sign_host || !y_mag_host ||
+        !y_sign_host || !status_host || !ws)
+        return HK_EINVAL;
+    if (((uintptr_t)ws & 255) != 0) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_STAGING, &pl);
+    if (rc) return rc;
+    if (ws_bytes < pl.info.ws_bytes_staging) return HK_ENOMEM;
+    cudaStream_t s = (cudaStream_t)stream;
+    char *base = (char *)ws;
+    const size_t L = pl.info.L, Ly = pl.info.Ly, na = pl.info.a_count;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    prm.a_mag = (const uint64_t *)(base + pl.st_amag);
+    prm.a_sign = (const int8_t *)(base + pl.st_asign);
+    prm.x_mag = (const uint64_t *)(base + pl.st_xmag);
+    prm.x_sign = (const int8_t *)(base + pl.st_xsign);
+    prm.y_mag = (uint64_t *)(base + pl.st_ymag);
+    prm.y_sign = (int8_t *)(base + pl.st_ysign);
+    const cudaMemcpyKind h2d = cudaMemcpyHostToDevice, d2h = cudaMemcpyDeviceToHost;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), s) != cudaSuccess ||
+        cudaMemcpyAsync((void *)prm.x_mag, x_mag_host, (size_t)n * L * 8, h2d, s) != cudaSuccess ||
+        cudaMemcpyAsync((void *)prm.x_sign, x_sign_host, (size_t)n, h2d, s) != cudaSuccess ||
+        cudaMemcpyAsync((void *)prm.a_mag, a_mag_host, na * L * 8, h2d, s) != cudaSuccess ||
+        cudaMemcpyAsync((void *)prm.a_sign, a_sign_host, na, h2d, s) != cudaSuccess)
+        return HK_ECUDA;
+    if ((rc = launch_ntt_path(prm, stream, HK_STAGE_ALL))) return rc;
+    if (cudaMemcpyAsync(y_mag_host, prm.y_mag, (size_t)m * Ly * 8, d2h, s) != cudaSuccess ||
+        cudaMemcpyAsync(y_sign_host, prm.y_sign, (size_t)m, d2h, s) != cudaSuccess ||
+        cudaMemcpyAsync(status_host, &prm.hdr->status, sizeof(int32_t), d2h, s) != cudaSuccess)
+        return HK_ECUDA;
+    return HK_OK;
+}
+
 int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                      const int8_t *a_sign, void *ws, size_t ws_bytes, void *stream) {
     if (!a_mag || !a_sign || !ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;

@@ -115,6 +115,45 @@ def test_host_buffer_path(hk, kind, n):
     assert_same((ym, ys), oracle.matvec(kind, 5000, am, asg, xm, xsg), "host path")
 
 
+@pytest.mark.parametrize("kind,n,P", [(0, 200, 5000), (1, 77, 3328), (2, 128, 1000), (2, 33, 700)])
+def test_host_pipeline_async(hk, kind, n, P):
+    """hk_matvec_host_async through HostPipeline: 7 different problems over 3 lanes in flight."""
+    import torch
+    pipe = hk.HostPipeline(kind, n, P, depth=3)
+    Ly = hk.out_limbs(P)
+    cases, outs = [], []
+    for t in range(7):
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=100 + t,
+                                           recipe="carry_stress" if t % 2 else "uniform")
+        host = [torch.from_numpy(v.view(np.int64) if v.dtype == np.uint64 else v).pin_memory()
+                for v in (am, asg, xm, xsg)]
+        out = (torch.empty((n, Ly), dtype=torch.int64).pin_memory(),
+               torch.empty((n,), dtype=torch.int8).pin_memory())
+        pipe.submit(*host, out)
+        cases.append((am, asg, xm, xsg, host))
+        outs.append(out)
+    pipe.drain()
+    for (am, asg, xm, xsg, _), (ym, ys) in zip(cases, outs):
+        got = (ym.numpy().view(np.uint64), ys.numpy())
+        assert_same(got, oracle.matvec(kind, P, am, asg, xm, xsg), "host pipeline")
+
+
+def test_host_pipeline_reports_data_error(hk):
+    import torch
+    n, P = 40, 200
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=5)
+    xm = xm.copy()
+    xm[3, -1] |= np.uint64(1) << np.uint64(63)  # bit >= P set
+    pipe = hk.HostPipeline(0, n, P, depth=2)
+    host = [torch.from_numpy(v.view(np.int64) if v.dtype == np.uint64 else v).pin_memory()
+            for v in (am, asg, xm, xsg)]
+    out = (torch.empty((n, hk.out_limbs(P)), dtype=torch.int64).pin_memory(),
+           torch.empty((n,), dtype=torch.int8).pin_memory())
+    pipe.submit(*host, out)
+    with pytest.raises(hk.HKError):
+        pipe.drain()
+
+
 def test_workspace_reuse_and_determinism(hk):
     am, asg, xm, xsg = gen.make_inputs(0, 500, 8000, seed=12)
     ws = hk.Workspace(0, 500, 8000)

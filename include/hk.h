@@ -179,6 +179,49 @@ int32_t hk_matvec_host_async(int32_t kind, int64_t m, int64_t n, int32_t P,
                              uint64_t *y_mag_host, int8_t *y_sign_host, int32_t *status_host,
                              void *ws, size_t ws_bytes, void *stream);
 
+/* ---- Multi-GPU: sigma-coset sharding (SURVEY.md 8(e) plan P-2) ------------------------------
+ * The 2-D convolution is split over G = 2, 4 or 8 ranks along the slice-transform dimension
+ * (the only coupling between slice frequencies sigma is the slice transform at each end):
+ *   rank g: hk_hankel_shard_forward -- slices every entry of a and x (replicated inputs) but
+ *           produces only block g of the G blocks of N2/G consecutive (bit-reversed order)
+ *           slice-transform outputs per entry, i.e. the frequencies = bitrev(g) mod G (the
+ *           coset fold: the first log2 G DIF stages keep one half each), runs the matrix-index
+ *           transforms, pointwise product and inverse on its 5 N2/G columns, and writes them into
+ *           `send` as G chunks [dest rank r][prime][column][rows_per_rank], chunk r holding the
+ *           output rows [r rpr, (r+1) rpr);
+ *   all ranks: an all-to-all of the chunks (chunk_words each; torch.distributed over NCCL);
+ *   rank g: hk_hankel_shard_finish -- with `recv` = [source rank][prime][column][rpr], the
+ *           inverse slice transforms of its rows, Garner CRT, carries, sign-magnitude, written into
+ *           rows [g rpr, g rpr + rpr) of the padded y buffer (y_rows = G rpr rows);
+ *   all ranks: an all-gather of those equal-size row blocks in rank order.  The final y is rows
+ *           [0, n) of the padded buffer (Hankel, circulant) or rows [y_rows - n, y_rows)
+ *           (Toeplitz, whose reversed rows are routed to ranks in reverse block order).
+ * Bit-identical to the single-GPU call.  Workspaces: hk_shard_plan(...).ws_bytes, initialised by
+ * hk_shard_workspace_init; one per rank.  All pointers are DEVICE pointers of the calling rank. */
+typedef struct {
+    int32_t G;              /* ranks (2, 4 or 8)                                                */
+    int32_t gamma;          /* log2 G                                                           */
+    int64_t block_cols;     /* slice-transform columns per prime per rank = N2 / G              */
+    int64_t rows_per_rank;  /* rpr: output rows per rank block (multiple of 4)                  */
+    int64_t y_rows;         /* rows of the padded y buffer = G rpr                              */
+    int64_t chunk_words;    /* uint32 words per all-to-all chunk = 5 block_cols rpr             */
+    int64_t buffer_words;   /* send / recv buffer words = G chunk_words                        */
+    uint64_t ws_bytes;      /* per-rank workspace bytes                                         */
+} hk_shard_info;
+
+int32_t hk_shard_plan(int32_t kind, int64_t n, int32_t P, int32_t G, hk_shard_info *out);
+int32_t hk_shard_workspace_init(int32_t kind, int64_t n, int32_t P, int32_t G, void *ws,
+                                size_t ws_bytes, void *stream);
+/* Phase 1 of rank g (see above).  a, x: DEVICE pointers (full, replicated); send: buffer_words. */
+int32_t hk_hankel_shard_forward(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                const uint64_t *a_mag, const int8_t *a_sign,
+                                const uint64_t *x_mag, const int8_t *x_sign, uint32_t *send,
+                                void *ws, size_t ws_bytes, void *stream);
+/* Phase 2 of rank g after the all-to-all: recv (buffer_words), y_mag[y_rows][Ly], y_sign[y_rows]. */
+int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                               const uint32_t *recv, uint64_t *y_mag, int8_t *y_sign, void *ws,
+                               size_t ws_bytes, void *stream);
+
 /* Pipeline stages of the NTT path, for per-kernel timing (bench.py) and phase-wise use:
  *   HK_STAGE_SLICE_ROWS  K1: validation, slicing, slice-dimension forward NTT of a and x
  *   HK_STAGE_COLUMNS     K2: matrix-index forward NTTs, pointwise product, inverse NTT

@@ -48,6 +48,17 @@ class PlanInfo(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ShardInfo(ctypes.Structure):
+    """hk_shard_info (include/hk.h): sigma-coset sharding layout."""
+    _fields_ = [("G", ctypes.c_int32), ("gamma", ctypes.c_int32), ("block_cols", ctypes.c_int64),
+                ("rows_per_rank", ctypes.c_int64), ("y_rows", ctypes.c_int64),
+                ("chunk_words", ctypes.c_int64), ("buffer_words", ctypes.c_int64),
+                ("ws_bytes", ctypes.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 def _load():
     if not os.path.exists(_LIB_PATH):
         raise ImportError(
@@ -73,6 +84,10 @@ def _load():
                                    vp, sz, vp]),
         "hk_karatsuba_workspace_size": (i32, [i64, i32, i32, ctypes.POINTER(sz)]),
         "hk_prepare_a": (i32, [i32, i64, i64, i32, vp, vp, vp, sz, vp]),
+        "hk_shard_plan": (i32, [i32, i64, i32, i32, ctypes.POINTER(ShardInfo)]),
+        "hk_shard_workspace_init": (i32, [i32, i64, i32, i32, vp, sz, vp]),
+        "hk_hankel_shard_forward": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_finish": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_prepared": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     }
@@ -88,7 +103,8 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_workspace_init", "hk_workspace_status", "hk_hankel_matvec", "hk_toeplitz_matvec",
             "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host", "hk_matvec_host_async",
             "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
-            "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared")
+            "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared", "hk_shard_plan",
+            "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -314,6 +330,58 @@ class HostPipeline:
                 ev.synchronize()
                 self._check_lane(lane)
                 self.events[lane] = None
+
+
+# ---- sigma-coset sharding phases (include/hk.h; orchestration in paper_1402_5287_b200.dist)
+def shard_plan(kind, n, P, G) -> dict:
+    info = ShardInfo()
+    _check(_lib.hk_shard_plan(int(kind), int(n), int(P), int(G), ctypes.byref(info)), "hk_shard_plan")
+    return info.as_dict()
+
+
+class ShardWorkspace:
+    """Per-rank device workspace of the sigma-coset sharded path."""
+
+    def __init__(self, kind, n, P, G, device=None, stream=None):
+        import torch
+        self.kind, self.n, self.P, self.G = int(kind), int(n), int(P), int(G)
+        self.info = shard_plan(kind, n, P, G)
+        self.nbytes = int(self.info["ws_bytes"])
+        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8,
+                               device=device or torch.device("cuda", torch.cuda.current_device()))
+        self.ptr = (self.buf.data_ptr() + 255) & ~255
+        _check(_lib.hk_shard_workspace_init(self.kind, self.n, self.P, self.G, self.ptr, self.nbytes,
+                                            _stream_ptr(stream)), "hk_shard_workspace_init")
+
+    def status(self, stream=None) -> int:
+        v = ctypes.c_int32()
+        _check(_lib.hk_workspace_status(self.ptr, _stream_ptr(stream), ctypes.byref(v)),
+               "hk_workspace_status")
+        return int(v.value)
+
+
+def shard_forward(ws: ShardWorkspace, g, a_mag, a_sign, x_mag, x_sign, send, stream=None):
+    """Phase 1 of rank g: send (int32 CUDA tensor of buffer_words) <- G all-to-all chunks."""
+    import torch
+    L, na = limbs(ws.P), (ws.n if ws.kind == CIRCULANT else 2 * ws.n - 1)
+    ptrs = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (ws.n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (ws.n,), "x_sign"),
+            _dev_ptr(send, (torch.int32,), (ws.info["buffer_words"],), "send")]
+    _check(_lib.hk_hankel_shard_forward(ws.kind, ws.n, ws.P, ws.G, int(g), *ptrs, ws.ptr,
+                                        ws.nbytes, _stream_ptr(stream)), "hk_hankel_shard_forward")
+
+
+def shard_finish(ws: ShardWorkspace, g, recv, y_mag, y_sign, stream=None):
+    """Phase 2 of rank g: rows [g rpr, (g+1) rpr) of the padded y (y_rows rows) from recv."""
+    import torch
+    yr, Ly = ws.info["y_rows"], out_limbs(ws.P)
+    ptrs = [_dev_ptr(recv, (torch.int32,), (ws.info["buffer_words"],), "recv"),
+            _dev_ptr(y_mag, _mag_dtypes(), (yr, Ly), "y_mag"),
+            _dev_ptr(y_sign, (torch.int8,), (yr,), "y_sign")]
+    _check(_lib.hk_hankel_shard_finish(ws.kind, ws.n, ws.P, ws.G, int(g), *ptrs, ws.ptr, ws.nbytes,
+                                       _stream_ptr(stream)), "hk_hankel_shard_finish")
 
 
 class Problem:

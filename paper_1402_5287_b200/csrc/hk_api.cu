@@ -78,7 +78,7 @@ Big big_pow2_minus1(int w) {  // 2^w - 1
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Plan *pl) {
+int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Plan *pl, int32_t G = 1) {
     if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || m < 1 || P < 1) return HK_EINVAL;
     if (kind != HK_HANKEL && m != n) return HK_EINVAL;
     std::memset(pl, 0, sizeof(*pl));
@@ -141,25 +141,26 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
         }
     }
     if (!found) return HK_EUNSUPPORTED;
+    // sigma-coset shards: G = 2^gamma <= 8 blocks of the slice transform (N2 / G >= 32)
+    if (G < 1 || G > 8 || (G & (G - 1)) || (int64_t(1) << in.log_n2) / G < 32) return HK_EUNSUPPORTED;
+    pl->G = G;
+    pl->gamma = G == 1 ? 0 : (G == 2 ? 1 : (G == 4 ? 2 : 3));
+    pl->rpr = G == 1 ? 0 : ((m + G - 1) / G + 3) / 4 * 4;
     const int64_t N2 = int64_t(1) << in.log_n2;
-    const int64_t S2 = 2 * (int64_t)in.Ls - 1;
+    const int64_t N2loc = N2 / G;
     pl->ldA = (in.a_count + 31) / 32 * 32;
     pl->ldX = (n + 31) / 32 * 32;
     pl->ldY = (m + 31) / 32 * 32;
-    pl->ldS = (S2 + 3) / 4 * 4;
     const int64_t N1 = int64_t(1) << in.log_n1;
     size_t off = align256(sizeof(WsHeader));
     pl->off_tw = off;
     off = align256(off + (size_t)kNumPrimes * (N1 + N2) * sizeof(uint2));
     pl->off_A = off;
-    size_t szA = (size_t)kNumPrimes * N2 * pl->ldA * 4;
-    const size_t szRes = (size_t)m * kNumPrimes * pl->ldS * 4;  // Yres aliases A^
-    if (szRes > szA) szA = szRes;
-    off = align256(off + szA);
+    off = align256(off + (size_t)kNumPrimes * N2loc * pl->ldA * 4);
     pl->off_X = off;
-    off = align256(off + (size_t)kNumPrimes * N2 * pl->ldX * 4);
-    pl->off_Y = off;
-    off = align256(off + (size_t)kNumPrimes * N2 * pl->ldY * 4);
+    off = align256(off + (size_t)kNumPrimes * N2loc * pl->ldX * 4);
+    pl->off_Y = off;  // sharded: K2 writes the caller's all-to-all send buffer instead
+    if (G == 1) off = align256(off + (size_t)kNumPrimes * N2 * pl->ldY * 4);
     pl->off_end = off;
     pl->off_stage = off;
     const size_t L = in.L, Ly = in.Ly;
@@ -181,12 +182,13 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     return HK_OK;
 }
 
-uint64_t plan_hash(int32_t kind, int64_t m, int64_t n, int32_t P) {
+uint64_t plan_hash(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t G = 1) {
     uint64_t h = 1469598103934665603ull;
     auto mix = [&](uint64_t v) {
         for (int i = 0; i < 8; ++i) { h ^= (v >> (8 * i)) & 0xff; h *= 1099511628211ull; }
     };
     mix((uint64_t)kind); mix((uint64_t)m); mix((uint64_t)n); mix((uint64_t)P);
+    if (G != 1) mix(0x5348415244ull + (uint64_t)G);  // "SHARD" + G
     return h;
 }
 
@@ -201,13 +203,17 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
     prm->cyclic = in.cyclic; prm->fold = in.fold;
     prm->reverse_out = pl.reverse_out; prm->x_reversed = pl.x_reversed;
     prm->out_off = pl.out_off;
-    prm->ldA = pl.ldA; prm->ldX = pl.ldX; prm->ldY = pl.ldY; prm->ldS = pl.ldS;
-    prm->hash = plan_hash(in.kind, in.m, in.n, in.P);
+    prm->ldA = pl.ldA; prm->ldX = pl.ldX; prm->ldY = pl.ldY;
+    prm->n2loc = prm->N2 / pl.G;
+    prm->log_n2loc = in.log_n2 - pl.gamma;
+    prm->shard_gamma = pl.gamma;
+    prm->shard_rpr = pl.rpr;
+    prm->y_rows = pl.G == 1 ? in.m : (int64_t)pl.G * pl.rpr;
+    prm->hash = plan_hash(in.kind, in.m, in.n, in.P, pl.G);
     char *base = (char *)ws;
     prm->hdr = (WsHeader *)base;
     prm->tw = (const uint2 *)(base + pl.off_tw);
     prm->Ahat = (uint32_t *)(base + pl.off_A);
-    prm->Yres = (uint32_t *)(base + pl.off_A);
     prm->Xhat = (uint32_t *)(base + pl.off_X);
     prm->Yhat = (uint32_t *)(base + pl.off_Y);
     const uint64_t N12 = (uint64_t)prm->N1 * (uint64_t)prm->N2;
@@ -522,6 +528,81 @@ int32_t hk_matvec_host_async(int32_t kind, int64_t m, int64_t n, int32_t P,
         cudaMemcpyAsync(status_host, &prm.hdr->status, sizeof(int32_t), d2h, s) != cudaSuccess)
         return HK_ECUDA;
     return HK_OK;
+}
+
+// ---- sigma-coset sharding (SURVEY.md 8(e) plan P-2)
+int32_t hk_shard_plan(int32_t kind, int64_t n, int32_t P, int32_t G, hk_shard_info *out) {
+    if (!out) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, n, n, P, 0, &pl, G);
+    if (rc) return rc;
+    out->G = G;
+    out->gamma = pl.gamma;
+    out->block_cols = (int64_t(1) << pl.info.log_n2) / G;
+    out->rows_per_rank = pl.rpr;
+    out->y_rows = (int64_t)G * pl.rpr;
+    out->chunk_words = (int64_t)kNumPrimes * out->block_cols * pl.rpr;
+    out->buffer_words = (int64_t)G * out->chunk_words;
+    out->ws_bytes = pl.info.ws_bytes;
+    return HK_OK;
+}
+
+int32_t hk_shard_workspace_init(int32_t kind, int64_t n, int32_t P, int32_t G, void *ws,
+                                size_t ws_bytes, void *stream) {
+    if (!ws || ((uintptr_t)ws & 255) != 0 || G < 2) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, n, n, P, 0, &pl, G);
+    if (rc) return rc;
+    if (ws_bytes < pl.info.ws_bytes) return HK_ENOMEM;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    uint32_t gens[kNumPrimes];
+    for (int k = 0; k < kNumPrimes; ++k) gens[k] = primitive_root(kPrimesHost[k]);
+    return launch_init(prm, gens, stream);
+}
+
+static int shard_common(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g, void *ws,
+                        size_t ws_bytes, Plan *pl, Params *prm) {
+    if (!ws || ((uintptr_t)ws & 255) != 0 || G < 2 || g < 0 || g >= G) return HK_EINVAL;
+    int rc = make_plan(kind, n, n, P, 0, pl, G);
+    if (rc) return rc;
+    if (ws_bytes < pl->info.ws_bytes) return HK_ENOMEM;
+    fill_params(*pl, ws, prm);
+    prm->k1_block = g;  // rank g keeps output block g (frequencies = bitrev(g) mod G)
+    // internal rows finished here (rows reversed for Toeplitz: see yhat_at in hk_k2.cuh)
+    prm->shard_row0 = (int64_t)(pl->info.kind == HK_TOEPLITZ ? G - 1 - g : g) * pl->rpr;
+    return HK_OK;
+}
+
+int32_t hk_hankel_shard_forward(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                const uint64_t *a_mag, const int8_t *a_sign,
+                                const uint64_t *x_mag, const int8_t *x_sign, uint32_t *send,
+                                void *ws, size_t ws_bytes, void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !send) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
+    prm.Yhat = send;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    return launch_ntt_path(prm, stream, HK_STAGE_SLICE_ROWS | HK_STAGE_COLUMNS);
+}
+
+int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                               const uint32_t *recv, uint64_t *y_mag, int8_t *y_sign, void *ws,
+                               size_t ws_bytes, void *stream) {
+    if (!recv || !y_mag || !y_sign) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    prm.Yhat = const_cast<uint32_t *>(recv);
+    prm.y_mag = y_mag; prm.y_sign = y_sign;
+    const int64_t row0 = prm.shard_row0;
+    const int64_t nrows = (n - row0) < pl.rpr ? (n - row0) : pl.rpr;
+    return launch_k3_range(prm, stream, row0, nrows);
 }
 
 int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,

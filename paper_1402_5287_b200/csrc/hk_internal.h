@@ -49,10 +49,17 @@ struct Params {
     int32_t log_n1, log_n2, N1, N2;
     int32_t cyclic, fold, reverse_out, x_reversed;
     int64_t out_off;             // first needed index of the matrix-index convolution
-    int64_t ldA, ldX, ldY, ldS;  // leading dims (elements) of the transform-domain arrays
+    int64_t ldA, ldX, ldY;       // leading dims (elements) of the transform-domain arrays
     uint64_t hash;
     int32_t tile0;               // K1: first tile of this launch (combined [a tiles | x tiles] index)
     int64_t row0;                // K3: first output row of this launch
+    // sigma-coset sharding (SURVEY.md 8(e) plan P-2; 1 shard = the single-GPU path):
+    int32_t n2loc, log_n2loc;    // transform-domain columns per prime held here (N2 / G)
+    int32_t shard_gamma;         // log2 G (0: not sharded)
+    int32_t k1_block;            // K1: slice-transform output block b = bitrev_gamma(g) kept
+    int64_t shard_rpr;           // rows per rank block (multiple of 4); 0: not sharded
+    int64_t shard_row0;          // K3: first internal row of this rank's block (g * rpr)
+    int64_t y_rows;              // rows of the y buffer (m, or G * rpr when sharded)
     // inputs / outputs (device)
     const uint64_t *a_mag;
     const int8_t *a_sign;
@@ -63,7 +70,8 @@ struct Params {
     // workspace regions
     WsHeader *hdr;
     const uint2 *tw;             // per prime: [N2 forward table | N1 forward table]
-    uint32_t *Ahat, *Xhat, *Yhat, *Yres;
+    uint32_t *Ahat, *Xhat, *Yhat;  // K2 writes Yhat; K3 reads it (the all-to-all receive
+                                   // buffer when sharded)
     uint32_t *AT;                // prepared 2-D transform of a (HK_WS_PREPARED), or null
     int32_t need_a_ready;        // K1 (x tiles): require hdr->a_ready
     PrimeConsts pc[kNumPrimes];
@@ -72,9 +80,11 @@ struct Params {
 
 struct Plan {
     hk_plan_info info;
+    int32_t G, gamma;            // sigma-coset shards (1, 0 unless a shard plan)
+    int64_t rpr;                 // rows per rank block (shard plans)
     int64_t out_off;
     int32_t reverse_out, x_reversed;
-    int64_t ldA, ldX, ldY, ldS;
+    int64_t ldA, ldX, ldY;
     size_t off_tw, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
     size_t st_amag, st_asign, st_xmag, st_xsign, st_ymag, st_ysign;
     size_t off_AT, off_end_prepared;

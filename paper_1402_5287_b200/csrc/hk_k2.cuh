@@ -126,9 +126,21 @@ HK_DEV void dit_bottom_regs(uint32_t (&v)[1 << RL], const uint2 *tw, uint32_t p)
     }
 }
 
+// Y^ element (column cidx, output row i): the single-GPU layout [column][ldY], or, for sigma-coset
+// shards, the all-to-all send buffer [dest rank][column][rpr]: row block i / rpr goes to rank
+// i / rpr (to rank G - 1 - i / rpr when the rows are reversed, Toeplitz, so that every rank's
+// final y rows form block `rank` of the padded y and the all-gather is in rank order).
+template <bool SHARD>
+HK_DEV uint32_t *yhat_at(const Params &prm, size_t cidx, int i) {
+    if constexpr (!SHARD) return prm.Yhat + cidx * prm.ldY + i;
+    const unsigned rpr = (unsigned)prm.shard_rpr, blk = (unsigned)i / rpr;
+    const unsigned dst = prm.reverse_out ? (1u << prm.shard_gamma) - 1u - blk : blk;
+    return prm.Yhat + ((size_t)dst * kNumPrimes * prm.n2loc + cidx) * rpr + ((unsigned)i - blk * rpr);
+}
+
 // Top inverse pass (R = 5, S = N/32) with the result going to HBM (or back to smem for fold).
-template <class TW, int LOGN, int T>
-HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, uint32_t *__restrict__ yc,
+template <class TW, int LOGN, int T, bool SHARD = false>
+HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, const Params &prm, size_t cidx,
                        int mrows, int off, bool to_smem) {
     constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
     for (int j0 = threadIdx.x; j0 < S; j0 += T) {
@@ -152,7 +164,7 @@ HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, uint32_t *__re
 #pragma unroll
             for (int m = 0; m < G; ++m) {
                 const int i = (N - (j0 + m * S) - off) & (N - 1);  // output row of this position
-                if (i < mrows) __stcs(yc + i, v[m]);
+                if (i < mrows) __stcs(yhat_at<SHARD>(prm, cidx, i), v[m]);
             }
         }
     }
@@ -171,14 +183,14 @@ constexpr size_t k2_smem_bytes() {
                                : (size_t)padded_len(1 << LOGN1) * 4;
 }
 
-template <class TW, int LOGN1>
+template <class TW, int LOGN1, bool SHARD>
 HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
     using PL = ColPlan<LOGN1>;
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
     constexpr bool STAGE = k2_stage_a<LOGN1>();
     const int tid = threadIdx.x;
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
-    const size_t cidx = (size_t)kp * prm.N2 + sigma;
+    const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     uint32_t *sA = sm + k2_stage_off<LOGN1>();
     if constexpr (STAGE) {  // issue the A^ column copy now; consumed after X^'s transform
         const int na = (int)prm.a_count;
@@ -230,38 +242,36 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     }
     __syncthreads();
     K2DitMiddle<TW, LOGN1, RL>::run(sm, twf, p);
-    uint32_t *yc = prm.Yhat + cidx * prm.ldY;
     const int mrows = (int)prm.m, off = (int)prm.out_off;
     if (!prm.fold) {
-        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, false);
+        k2_dit_top<TW, LOGN1, T, SHARD>(sm, twf, p, prm, cidx, mrows, off, false);
     } else {  // circulant via linear convolution: y[i] = z[i] + z[i + n]
-        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, true);
+        k2_dit_top<TW, LOGN1, T, SHARD>(sm, twf, p, prm, cidx, mrows, off, true);
         const int nn = (int)prm.n;
         for (int i = tid; i < mrows; i += T) {
             const uint32_t v = sm[pad((N1 - (off + i)) & (N1 - 1))];
-            yc[i] = addm(v, sm[pad((N1 - (off + i + nn)) & (N1 - 1))], p);
+            *yhat_at<SHARD>(prm, cidx, i) = addm(v, sm[pad((N1 - (off + i + nn)) & (N1 - 1))], p);
         }
         __syncthreads();
     }
 }
 
 // Inverse passes above the bottom one, output to Y^ (shared by the full and prepared bodies).
-template <class TW, int LOGN1>
+template <class TW, int LOGN1, bool SHARD = false>
 HK_DEV void k2_inverse_tail(const Params &prm, uint32_t *sm, const uint2 *twf, uint32_t p,
                             size_t cidx) {
     using PL = ColPlan<LOGN1>;
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL;
     K2DitMiddle<TW, LOGN1, RL>::run(sm, twf, p);
-    uint32_t *yc = prm.Yhat + cidx * prm.ldY;
     const int mrows = (int)prm.m, off = (int)prm.out_off;
     if (!prm.fold) {
-        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, false);
+        k2_dit_top<TW, LOGN1, T, SHARD>(sm, twf, p, prm, cidx, mrows, off, false);
     } else {
-        k2_dit_top<TW, LOGN1, T>(sm, twf, p, yc, mrows, off, true);
+        k2_dit_top<TW, LOGN1, T, SHARD>(sm, twf, p, prm, cidx, mrows, off, true);
         const int nn = (int)prm.n;
         for (int i = threadIdx.x; i < mrows; i += T) {
             const uint32_t v = sm[pad((N1 - (off + i)) & (N1 - 1))];
-            yc[i] = addm(v, sm[pad((N1 - (off + i + nn)) & (N1 - 1))], p);
+            *yhat_at<SHARD>(prm, cidx, i) = addm(v, sm[pad((N1 - (off + i + nn)) & (N1 - 1))], p);
         }
         __syncthreads();
     }
@@ -275,7 +285,7 @@ HK_DEV void k2_prepare_body(const Params &prm, uint32_t *sm, const uint2 *twf, i
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
     const int tid = threadIdx.x;
     const uint32_t p = prm.pc[kp].p;
-    const size_t cidx = (size_t)kp * prm.N2 + sigma;
+    const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     const int na = (int)prm.a_count;
     k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm, twf, p);
     K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
@@ -299,7 +309,7 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
     const int tid = threadIdx.x;
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
-    const size_t cidx = (size_t)kp * prm.N2 + sigma;
+    const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     const int nx = (int)prm.n;
     k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx, nx <= N1 / 2, sm, twf, p);
     K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
@@ -324,16 +334,19 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
 }
 
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
-// MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT).
+// MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT);
+// 3: full column of a sigma-coset shard (output to the all-to-all send buffer).
 template <int LOGN1, class TW = TwGlobal, int MODE = 0>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
     const int col = blockIdx.x;
-    const int kp = col >> prm.log_n2;
+    const int kp = col >> prm.log_n2loc;  // columns (prime, sigma) held here: n2loc per prime
+    const int sigma = col & (prm.n2loc - 1);
     const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1) + prm.N2;
-    if constexpr (MODE == 0) k2_column_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
-    else if constexpr (MODE == 1) k2_prepare_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
-    else k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, col & (prm.N2 - 1));
+    if constexpr (MODE == 0) k2_column_body<TW, LOGN1, false>(prm, sm, twf, kp, sigma);
+    else if constexpr (MODE == 3) k2_column_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);
+    else if constexpr (MODE == 1) k2_prepare_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
+    else k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
 }
 
 }  // namespace hk

@@ -82,9 +82,18 @@ constexpr int k1_threads() {
     return kK1Rows * ((1 << LOGN2) / 32 > 8 ? (1 << LOGN2) / 32 : 8);
 }
 
-template <int LOGN2>
+// GAMMA > 0 (sigma-coset shards): only block b = prm.k1_block of the 2^GAMMA
+// blocks of N2 / 2^GAMMA consecutive outputs is produced.  After the first GAMMA DIF stages the
+// array splits into independent blocks; block b only needs, at stage h, the "sum" (bit 0) or the
+// "difference x twiddle" (bit 1) half selected by b's bits from the top -- i.e. the coset fold.
+// Block b holds the transform outputs at bit-reversed positions [b N2 / G, (b + 1) N2 / G), the
+// frequencies congruent to bitrev(b) mod G.
+template <int LOGN2, int GAMMA>
 __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params prm, int tiles_a) {
     constexpr int N2 = 1 << LOGN2;
+    constexpr int BL = N2 >> GAMMA;          // outputs kept per row and prime
+    constexpr int GK = 32 >> GAMMA;          // top-pass points kept per group
+    static_assert(BL >= 32, "shard blocks must hold >= 32 outputs");
     constexpr int RS = k1_row_stride<LOGN2>();
     constexpr int T = k1_threads<LOGN2>();
     constexpr int R1 = 5, G1 = 32, H1 = 16;  // top pass: 32 points, upper 16 are zero padding
@@ -206,33 +215,58 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
                 v[m] = res;
             }
             // top stage (h = N2/2) with a zero upper half: (u, 0) -> (u, u W)
+            if constexpr (GAMMA == 0) {
 #pragma unroll
-            for (int m = 0; m < H1; ++m) {
-                const uint2 wv = TwShared::ld(tw, S1 * H1 + j0 + S1 * m);
-                v[m + H1] = red1(shoup(v[m], wv.x, wv.y, p), p);
+                for (int m = 0; m < H1; ++m) {
+                    const uint2 wv = TwShared::ld(tw, S1 * H1 + j0 + S1 * m);
+                    v[m + H1] = red1(shoup(v[m], wv.x, wv.y, p), p);
+                }
+            } else {  // keep the half selected by the top bit of b (in v[0 .. 16))
+                if ((prm.k1_block >> (GAMMA - 1)) & 1) {
+#pragma unroll
+                    for (int m = 0; m < H1; ++m) {
+                        const uint2 wv = TwShared::ld(tw, S1 * H1 + j0 + S1 * m);
+                        v[m] = red1(shoup(v[m], wv.x, wv.y, p), p);
+                    }
+                }
+#pragma unroll
+                for (int l = 1; l < GAMMA; ++l) {  // stages h = N2/4 .. : keep one half each
+                    const int half = H1 >> l;
+                    const bool hi = (prm.k1_block >> (GAMMA - 1 - l)) & 1;
+#pragma unroll
+                    for (int m = 0; m < half; ++m) {
+                        const uint32_t u = v[m], w = v[m + half];
+                        if (hi) {
+                            const uint2 wv = TwShared::ld(tw, S1 * half + j0 + S1 * m);
+                            v[m] = red1(shoup(u - w + p, wv.x, wv.y, p), p);
+                        } else {
+                            v[m] = addm(u, w, p);
+                        }
+                    }
+                }
             }
 #pragma unroll
-            for (int l = R1 - 2; l >= 0; --l) {
+            for (int l = R1 - 2 - (GAMMA > 0 ? GAMMA - 1 : 0); l >= 0; --l) {
                 const int half = 1 << l;
 #pragma unroll
-                for (int m = 0; m < G1; ++m) {
+                for (int m = 0; m < GK; ++m) {
                     if (m & half) continue;
                     const uint2 wv = TwShared::ld(tw, S1 * half + j0 + S1 * (m & (half - 1)));
                     gs_bfly(v[m], v[m + half], wv, p);
                 }
             }
 #pragma unroll
-            for (int m = 0; m < G1; ++m) sm[r * RS + pad(j0 + m * S1)] = v[m];
+            for (int m = 0; m < GK; ++m) sm[r * RS + pad(j0 + m * S1)] = v[m];
         }
         __syncthreads();
         constexpr int REM = LOGN2 - R1;          // stages left after the top pass
         constexpr int RB = REM < 5 ? REM : 5;    // bottom pass (S = 1) radix
-        if constexpr (REM > RB)
-            dif_pass<TwShared, LOGN2, REM - RB, (1 << RB), false>(sm, kK1Rows, RS, tw, p, tid, T);
+        if constexpr (REM > RB)  // block-local (positions relative to the block start)
+            dif_pass<TwShared, LOGN2 - GAMMA, REM - RB, (1 << RB), false>(sm, kK1Rows, RS, tw, p, tid, T);
         // ---- bottom pass in registers, stored straight to [prime][sigma][row]; lanes cover
         // 8 rows x 4 groups so every store instruction writes full 32-byte row segments
         // (x rows reversed: matrix index n-1-row)
-        constexpr int GB = 1 << RB, NGR = N2 / GB;
+        constexpr int GB = 1 << RB, NGR = BL / GB;
         for (int gi = tid; gi < kK1Rows * NGR; gi += T) {
             const int rr = gi % kK1Rows, g = gi / kK1Rows;
             uint32_t v[GB];
@@ -242,7 +276,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
             const int64_t orow = r0 + rr;
             if (orow < count) {
                 const int64_t pos = rev ? (count - 1 - orow) : orow;
-                uint32_t *o = out + ((int64_t)kp * N2 + (int64_t)g * GB) * ld + pos;
+                uint32_t *o = out + ((int64_t)kp * BL + (int64_t)g * GB) * ld + pos;
 #pragma unroll
                 for (int m = 0; m < GB; ++m) o[(int64_t)m * ld] = v[m];
             }
@@ -403,7 +437,14 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
         const bool vec = r0 + R <= m && ((r0 & (R - 1)) == 0);
         for (int e = tid; e < kNumPrimes * N2; e += T) {
             const int kp = e >> LOGN2, sg = e & (N2 - 1);
-            const uint32_t *g = prm.Yhat + (int64_t)(kp * N2 + sg) * prm.ldY + r0;
+            const uint32_t *g;
+            if (prm.shard_gamma == 0) {
+                g = prm.Yhat + (int64_t)(kp * N2 + sg) * prm.ldY + r0;
+            } else {  // all-to-all receive buffer [source rank][prime][sigma-block column][rpr]
+                const int src = sg >> prm.log_n2loc, q = sg & (prm.n2loc - 1);  // rank src held block src
+                g = prm.Yhat + ((int64_t)(src * kNumPrimes + kp) * prm.n2loc + q) * prm.shard_rpr +
+                    (r0 - prm.shard_row0);
+            }
             uint32_t *d = sm + LY::idx(kp, sg, 0);
             if (vec) {
                 if constexpr (R == 4) cp_async16(d, g);
@@ -561,7 +602,7 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
     for (int rr = 0; rr < R; ++rr) {
         const int64_t orow_r = r0 + rr;
         if (orow_r >= m) break;
-        const int64_t orow = prm.reverse_out ? (m - 1 - orow_r) : orow_r;
+        const int64_t orow = prm.reverse_out ? (prm.y_rows - 1 - orow_r) : orow_r;
         uint64_t *yo = prm.y_mag + orow * Ly;
         for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
         if (tid == 0)
@@ -591,8 +632,8 @@ int launch_init(const Params &prm, const uint32_t *gens, void *stream) {
     return check_launch();
 }
 
-template <int LOGN2>
-static int launch_rows(const Params &prm0, cudaStream_t st, int tile0 = 0, int ntiles = -1) {
+template <int LOGN2, int GAMMA>
+static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int ntiles) {
     const int ga = (int)((prm0.a_count + kK1Rows - 1) / kK1Rows);
     const int gx = (int)((prm0.n + kK1Rows - 1) / kK1Rows);
     if (ntiles < 0) ntiles = ga + gx - tile0;
@@ -603,22 +644,37 @@ static int launch_rows(const Params &prm0, cudaStream_t st, int tile0 = 0, int n
     const size_t tab_bytes = (size_t)2 * (1 << LOGN2) * sizeof(uint2);  // 2 tables, reuse the limb area
     const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t) +
                          (limb_bytes > tab_bytes ? limb_bytes : tab_bytes);
-    if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2, GAMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess)
         return HK_ECUDA;
-    k1_slice_rowntt<LOGN2><<<ntiles, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
+    k1_slice_rowntt<LOGN2, GAMMA><<<ntiles, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();
 }
 
+template <int LOGN2>
+static int launch_rows(const Params &prm, cudaStream_t st, int tile0 = 0, int ntiles = -1) {
+    switch (prm.shard_gamma) {
+        case 0: return launch_rows_g<LOGN2, 0>(prm, st, tile0, ntiles);
+        case 1: if constexpr (LOGN2 >= 6) return launch_rows_g<LOGN2, 1>(prm, st, tile0, ntiles); break;
+        case 2: if constexpr (LOGN2 >= 7) return launch_rows_g<LOGN2, 2>(prm, st, tile0, ntiles); break;
+        case 3: if constexpr (LOGN2 >= 8) return launch_rows_g<LOGN2, 3>(prm, st, tile0, ntiles); break;
+    }
+    return HK_EUNSUPPORTED;
+}
+
+template <int LOGN1, int MODE>
+static int launch_cols_m(const Params &prm, cudaStream_t st) {
+    const int ncols = kNumPrimes * prm.n2loc;
+    const size_t smem = k2_smem_bytes<LOGN1>();
+    if (cudaFuncSetAttribute(k2_column<LOGN1, TwGlobal, MODE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    k2_column<LOGN1, TwGlobal, MODE><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
+    return check_launch();
+}
 template <int LOGN1>
 static int launch_cols(const Params &prm, cudaStream_t st) {
-    const int ncols = kNumPrimes * prm.N2;
-    const size_t smem = k2_smem_bytes<LOGN1>();
-    if (cudaFuncSetAttribute(k2_column<LOGN1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return HK_ECUDA;
-    k2_column<LOGN1><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
-    return check_launch();
+    return prm.shard_rpr ? launch_cols_m<LOGN1, 3>(prm, st) : launch_cols_m<LOGN1, 0>(prm, st);
 }
 
 int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
@@ -645,7 +701,7 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
 
 template <int LOGN1, int MODE>
 static int launch_cols_mode(const Params &prm, cudaStream_t st) {
-    const int ncols = kNumPrimes * prm.N2;
+    const int ncols = kNumPrimes * prm.n2loc;
     const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
     if (cudaFuncSetAttribute(k2_column<LOGN1, TwGlobal, MODE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

@@ -1,5 +1,12 @@
-"""Multi-GPU Hankel matvec: row-block sharding with an all-gather of y (BASELINE north_star;
-SURVEY.md 8(e) plan P-3).
+"""Multi-GPU matvec, one process per GPU, torch.distributed for the plumbing.
+
+* CosetShardedMatvec -- plan P-2 (sigma-coset sharding, the recommended plan): rank g produces
+  only block g of the slice-transform outputs of every entry (coset fold inside K1), runs K2 on
+  its N2/G columns per prime and writes per-destination row-block chunks; one all-to-all moves
+  Y^ from column ownership to row ownership; rank g finishes its row block (K3); an all-gather of
+  the equal-size y blocks gives every rank y.  Compute per rank ~1/G of K2/K3 and of K1's
+  transforms (slicing is replicated).
+* ShardedHankel -- plan P-3, north_star's literal row-block sharding (below).
 
 One process per GPU (torchrun), torch.distributed for the plumbing (NCCL over NVLink on GPUs,
 gloo in the CPU tests).  Rank g owns output rows [r0, r0 + nr) of the n x n Hankel product; its
@@ -104,3 +111,89 @@ class ShardedHankel:
 def hankel_matvec(a_mag, a_sign, x_mag, x_sign, P, group=None, compute=None):
     """y = A_H x sharded by rows over the process group; returns the full y on every rank."""
     return ShardedHankel(a_mag, a_sign, x_mag, x_sign, P, group=group, compute=compute).step()
+
+
+# ---------------------------------------------------------------------------------------------
+# plan P-2: sigma-coset sharding
+def _cuda_forward(ws, g, a_mag, a_sign, x_mag, x_sign, send):
+    from . import shard_forward
+    shard_forward(ws, g, a_mag, a_sign, x_mag, x_sign, send)
+
+
+def _cuda_finish(ws, g, recv, y_mag, y_sign):
+    from . import shard_finish
+    shard_finish(ws, g, recv, y_mag, y_sign)
+
+
+class CosetShardedMatvec:
+    """Prepared sigma-coset-sharded problem (kind in {Hankel, Toeplitz, circulant}, n x n) for
+    repeated steps: rank-local workspace, all-to-all send / receive buffers and the padded y.
+
+    ``forward(ws, g, a, sa, x, sx, send)`` and ``finish(ws, g, recv, y, s)`` default to the CUDA
+    phases (hk_hankel_shard_forward / _finish); tests inject stand-ins to exercise the exchange
+    on CPU (gloo), with ``info`` the layout (paper_1402_5287_b200.shard_plan)."""
+
+    def __init__(self, kind, a_mag, a_sign, x_mag, x_sign, P, group=None, forward=None,
+                 finish=None, info=None):
+        import torch
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.G = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.kind, self.P = int(kind), int(P)
+        self.n = int(x_mag.shape[0])
+        self.inputs = (a_mag, a_sign, x_mag, x_sign)
+        dev = a_mag.device
+        self.ws = None
+        if forward is None or finish is None:
+            from . import ShardWorkspace
+            self.ws = ShardWorkspace(kind, self.n, P, self.G, device=dev)
+            info = self.ws.info
+        self.info = info
+        self.forward = forward or _cuda_forward
+        self.finish = finish or _cuda_finish
+        words, rpr, yr = info["buffer_words"], info["rows_per_rank"], info["y_rows"]
+        self.rpr, self.y_rows = int(rpr), int(yr)
+        Ly = 2 * ((P + 63) // 64) + 1
+        self.send = torch.zeros((words,), dtype=torch.int32, device=dev)
+        self.recv = torch.zeros((words,), dtype=torch.int32, device=dev)
+        self.y_pad = torch.zeros((yr, Ly), dtype=a_mag.dtype, device=dev)
+        self.s_pad = torch.zeros((yr,), dtype=torch.int8, device=dev)
+
+    def compute_forward(self):
+        self.forward(self.ws, self.rank, *self.inputs, self.send)
+
+    def exchange(self):
+        self.dist.all_to_all_single(self.recv, self.send, group=self.group)
+
+    def compute_finish(self):
+        self.finish(self.ws, self.rank, self.recv, self.y_pad, self.s_pad)
+
+    def gather(self):
+        r0, r1 = self.rank * self.rpr, (self.rank + 1) * self.rpr
+        d = self.dist
+        try:  # in place: this rank's block already sits in its slot of the output
+            d.all_gather_into_tensor(self.y_pad, self.y_pad[r0:r1], group=self.group)
+            d.all_gather_into_tensor(self.s_pad, self.s_pad[r0:r1], group=self.group)
+        except (RuntimeError, NotImplementedError, AttributeError):  # backends without it
+            ym, ys = self.y_pad[r0:r1].clone(), self.s_pad[r0:r1].clone()
+            d.all_gather(list(self.y_pad.chunk(self.G)), ym, group=self.group)
+            d.all_gather(list(self.s_pad.chunk(self.G)), ys, group=self.group)
+
+    def result(self):
+        """The final y (views of the padded buffer): rows [0, n), or the last n for Toeplitz."""
+        if self.kind == 1:  # Toeplitz: reversed rows are padded at the front
+            return self.y_pad[self.y_rows - self.n:], self.s_pad[self.y_rows - self.n:]
+        return self.y_pad[: self.n], self.s_pad[: self.n]
+
+    def step(self):
+        self.compute_forward()
+        self.exchange()
+        self.compute_finish()
+        self.gather()
+        return self.result()
+
+
+def coset_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, group=None):
+    """y = A x over the process group with plan P-2; returns the full y on every rank."""
+    return CosetShardedMatvec(kind, a_mag, a_sign, x_mag, x_sign, P, group=group).step()

@@ -81,3 +81,77 @@ def test_sharded_matvec_gloo_world2(n):
     wm, ws = oracle.matvec(0, P, am, asg, xm, xsg, threads=2)
     for _, ym, ys in res:
         assert np.array_equal(ym, wm) and np.array_equal(ys, ws)
+
+
+# ---------------------------------------------------------------------------------------------
+# plan P-2 (sigma-coset sharding): exchange and gather logic of CosetShardedMatvec on CPU.
+# The CUDA phases are replaced by stand-ins that write / check labelled words, so the test pins
+# the all-to-all chunk routing, the in-place all-gather of the padded y, and the Toeplitz layout.
+def _label(src, dst, j):
+    return (src * 7919 + dst * 104729 + j) % (2 ** 31 - 1)
+
+
+def _coset_worker(rank, world, port, kind, n, P, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1402_5287_b200 as hk
+        info = hk.shard_plan(kind, n, P, world)  # host-side planner, no GPU needed
+        chunk, rpr = info["chunk_words"], info["rows_per_rank"]
+        j = torch.arange(chunk, dtype=torch.int64)
+
+        def forward(ws, g, am, asg, xm, xsg, send):
+            for dst in range(world):
+                send[dst * chunk:(dst + 1) * chunk] = torch.tensor(
+                    [_label(g, dst, int(v)) for v in j[:3]] + [0] * (chunk - 3), dtype=torch.int32)
+
+        seen = {}
+
+        def finish(ws, g, recv, y_mag, y_sign):
+            for src in range(world):
+                seen[src] = [int(v) for v in recv[src * chunk:src * chunk + 3]]
+            y_mag[g * rpr:(g + 1) * rpr] = 1000 + g
+            y_sign[g * rpr:(g + 1) * rpr] = g + 1
+
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=1)
+        t = [torch.from_numpy(am.view(np.int64)), torch.from_numpy(asg),
+             torch.from_numpy(xm.view(np.int64)), torch.from_numpy(xsg)]
+        from paper_1402_5287_b200 import dist as hd
+        sh = hd.CosetShardedMatvec(kind, *t, P, forward=forward, finish=finish, info=info)
+        ym, ys = sh.step()
+        q.put((rank, seen, sh.y_pad.numpy().copy(), sh.s_pad.numpy().copy(), ym.shape[0],
+               int(ym[0, 0]), int(ym[-1, 0])))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,n,P", [(0, 101, 4200), (1, 101, 4200), (2, 64, 4200)])
+def test_coset_exchange_gloo_world2(kind, n, P):
+    import paper_1402_5287_b200 as hk
+    world = 2
+    info = hk.shard_plan(kind, n, P, world)
+    rpr, yr = info["rows_per_rank"], info["y_rows"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_coset_worker, args=(r, world, port, kind, n, P, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, seen, y_pad, s_pad, nrows, first, last in res:
+        # all-to-all: chunk src of rank r's receive buffer is chunk r of rank src's send buffer
+        for src in range(world):
+            assert seen[src] == [_label(src, rank, v) for v in range(3)]
+        # all-gather: block g of the padded y comes from rank g, on every rank
+        for g in range(world):
+            assert (y_pad[g * rpr:(g + 1) * rpr] == 1000 + g).all()
+            assert (s_pad[g * rpr:(g + 1) * rpr] == g + 1).all()
+        assert nrows == n and yr >= n
+        if kind == 1:  # Toeplitz: final rows are the LAST n rows of the padded buffer
+            assert last == 1000 + world - 1 and first == 1000 + (yr - n) // rpr
+        else:
+            assert first == 1000 and last == 1000 + (n - 1) // rpr

@@ -1,0 +1,95 @@
+"""GPU parity of the sigma-coset sharded path (SURVEY.md 8(e) plan P-2) through the C ABI
+(hk_hankel_shard_forward / hk_hankel_shard_finish), bit-exact against the oracle.
+
+There is one GPU here, so the G ranks run one after another in this process and the all-to-all
+and all-gather are emulated by copies between their buffers (the same layouts NCCL moves in
+paper_1402_5287_b200.dist.CosetShardedMatvec).  No rank waits on another inside a kernel."""
+import numpy as np
+import pytest
+
+import hkinputs as gen
+import oracle
+from tests import fingerprint as fp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def hk():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1402_5287_b200 as hk
+    return hk
+
+
+def sharded(hk, kind, G, am, asg, xm, xsg, P):
+    n = xm.shape[0]
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    wss = [hk.ShardWorkspace(kind, n, P, G) for _ in range(G)]
+    info = wss[0].info
+    chunk, rpr, yr = info["chunk_words"], info["rows_per_rank"], info["y_rows"]
+    Ly = hk.out_limbs(P)
+    send = [torch.full((info["buffer_words"],), -1, dtype=torch.int32, device="cuda") for _ in range(G)]
+    for g in range(G):
+        hk.shard_forward(wss[g], g, a, sa, x, sx, send[g])
+    # all-to-all: recv[r] chunk g = send[g] chunk r
+    recv = [torch.cat([send[g][r * chunk:(r + 1) * chunk] for g in range(G)]) for r in range(G)]
+    y_pads = []
+    for g in range(G):
+        ym = torch.full((yr, Ly), -7, dtype=torch.int64, device="cuda")
+        ys = torch.full((yr,), 9, dtype=torch.int8, device="cuda")
+        hk.shard_finish(wss[g], g, recv[g], ym, ys)
+        y_pads.append((ym, ys))
+    for g in range(G):
+        assert wss[g].status() == hk.HK_OK
+    # all-gather: block g of the padded y comes from rank g
+    ym = torch.cat([y_pads[g][0][g * rpr:(g + 1) * rpr] for g in range(G)])
+    ys = torch.cat([y_pads[g][1][g * rpr:(g + 1) * rpr] for g in range(G)])
+    torch.cuda.synchronize()
+    if kind == gen.TOEPLITZ:
+        ym, ys = ym[yr - n:], ys[yr - n:]
+    else:
+        ym, ys = ym[:n], ys[:n]
+    return hk.to_host(ym, ys)
+
+
+@pytest.mark.parametrize("kind,n,P,G", [
+    (0, 100, 4200, 2), (0, 100, 4200, 4), (0, 100, 4200, 8), (1, 77, 4200, 2), (1, 130, 8000, 8),
+    (2, 64, 4200, 4), (2, 77, 9000, 8), (0, 1, 4200, 2), (0, 5, 17000, 8), (1, 3, 2500, 2),
+    (0, 257, 2100, 2), (2, 128, 2100, 4)])
+def test_coset_shards_match_oracle(hk, kind, n, P, G):
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=40 + n + G)
+    got = sharded(hk, kind, G, am, asg, xm, xsg, P)
+    want = oracle.matvec(kind, P, am, asg, xm, xsg)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_coset_shards_carry_stress(hk):
+    kind, n, P, G = 1, 96, 16608, 4
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=4, recipe="carry_stress")
+    got = sharded(hk, kind, G, am, asg, xm, xsg, P)
+    want = oracle.matvec(kind, P, am, asg, xm, xsg)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_coset_shards_c2_fingerprints(hk, G):
+    """BASELINE C2 (n = 1024, P = 33,216) over G shards: modular fingerprints of every row plus
+    the oracle on sampled rows."""
+    c = gen.CONFIGS["C2"]
+    am, asg, xm, xsg = gen.config_inputs("C2")
+    ym, ys = sharded(hk, c["kind"], G, am, asg, xm, xsg, c["P"])
+    fp.check(c["kind"], am, asg, xm, xsg, ym, ys)
+    rows = np.arange(0, c["n"], 97)
+    wm, ws = oracle.matvec(c["kind"], c["P"], am, asg, xm, xsg, rows=rows)
+    assert np.array_equal(ym[rows], wm) and np.array_equal(ys[rows], ws)
+
+
+def test_shard_plan_rejects_bad_G(hk):
+    for G in (3, 16, 0):
+        with pytest.raises(hk.HKError):
+            hk.shard_plan(0, 100, 4200, G)
+    with pytest.raises(hk.HKError):  # N2 / G < 32 (P = 1000 -> N2 = 32)
+        hk.shard_plan(0, 100, 1000, 2)

@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--config", default="C3", choices=sorted(gen.CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--plan", default="coset", choices=["coset", "rowblock"],
+                    help="multi-GPU plan (N > 1): SURVEY 8(e) P-2 sigma-coset (default) or P-3 row blocks")
     return ap.parse_args()
 
 
@@ -246,11 +248,35 @@ def main():
             prob.run(hk.STAGE_FINISH)
             e[3].record(stream)
         launches_per_step = 3  # K1 (a and x tiles), K2, K3
+    elif args.plan == "coset":
+        # SURVEY 8(e) plan P-2: coset-sharded K1/K2 -> NCCL all-to-all -> row-block K3 ->
+        # NCCL all-gather of y; stages: forward, all-to-all, finish + all-gather
+        from paper_1402_5287_b200 import dist as hkdist
+        sh = hkdist.CosetShardedMatvec(kind, a, sa, x, sx, P)
+        sh.step()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+        stage_names = ("shard_forward_K1K2", "all_to_all", "shard_finish_K3+all_gather")
+
+        def step(i=None):
+            if i is None:
+                sh.step()
+                return
+            e = ev[i]
+            e[0].record(stream)
+            sh.compute_forward()
+            e[1].record(stream)
+            sh.exchange()
+            e[2].record(stream)
+            sh.compute_finish()
+            sh.gather()
+            e[3].record(stream)
+        launches_per_step = 3  # K1 (coset block), K2 (N2/G columns), K3 (row block)
     else:
         from paper_1402_5287_b200 import dist as hkdist
         sh = hkdist.ShardedHankel(a, sa, x, sx, P)
         sh.step()
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+        stage_names = ("-", "shard_compute", "all_gather")
 
         def step(i=None):
             if i is None:
@@ -427,11 +453,12 @@ def main():
         "config": {"workload": wl["desc"], "kind": gen.KIND_NAMES[kind], "n": n, "P": P,
                    "plan": {k: plan[k] for k in ("w", "Ls", "log_n1", "log_n2", "k_primes",
                                                  "margin_bits")},
-                   "parallelism": "single GPU" if world == 1 else f"row-block x{world} + NCCL all-gather",
+                   "parallelism": "single GPU" if world == 1 else (
+                       f"sigma-coset x{world}: NCCL all-to-all + all-gather" if args.plan == "coset"
+                       else f"row-block x{world} + NCCL all-gather"),
                    "l2": "no flush: per-step working set (inputs 100 MB + transform-domain "
                          f"{all_bytes / 1e6:.0f} MB traffic) exceeds the 126 MB L2"},
-        "stages_ms": dict(zip(stage_names if world == 1 else ("-", "shard_compute", "all_gather"),
-                              stage_ms)),
+        "stages_ms": dict(zip(stage_names, stage_ms)),
         "roofline": roof,
         "cpu_baseline": cb,
         "e2e": e2e,

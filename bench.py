@@ -350,6 +350,30 @@ def main():
                         "per step: x slicing + transforms, pointwise, inverse, CRT, carry"}
         del A
 
+    # ---- F4 (secondary): the same matvec with y rounded back to the input format (L+1 limbs)
+    rounded = None
+    if rank == 0 and world == 1:
+        L = plan["L"]
+        yr = (torch.empty((n, L + 1), dtype=torch.int64, device=dev),
+              torch.empty((n,), dtype=torch.int8, device=dev))
+        wsr = hk.Workspace(kind, n, P)
+        for _ in range(W):
+            hk.matvec(kind, a, sa, x, sx, P, out=yr, ws=wsr, check=False, rounded=True)
+        torch.cuda.synchronize()
+        r0_ = torch.cuda.Event(enable_timing=True)
+        r1_ = torch.cuda.Event(enable_timing=True)
+        r0_.record(stream)
+        for _ in range(K):
+            hk.matvec(kind, a, sa, x, sx, P, out=yr, ws=wsr, check=False, rounded=True)
+        r1_.record(stream)
+        torch.cuda.synchronize()
+        if wsr.status() != hk.HK_OK:
+            raise SystemExit("bench: rounded-matvec status not OK")
+        rms = r0_.elapsed_time(r1_) / K
+        rounded = {"value": 1000.0 / rms, "unit": UNIT, "ms_per_step": rms,
+                   "what": "hk_matvec_rounded: y = round_half_even(Y / 2^P), L+1 limbs (SURVEY 8(f) F4)"}
+        del wsr, yr
+
     # ---- e2e through the host-buffer C-ABI call (N = 1 workload per rank)
     e2e = None
     if rank == 0 and not args.no_e2e and world == 1:
@@ -463,6 +487,7 @@ def main():
         "cpu_baseline": cb,
         "e2e": e2e,
         "warm_a": warm,
+        "rounded": rounded,
         "gpu_launches": launches_per_step * K,
         "clocks": clocks,
         "library": hk.library_path(),

@@ -152,6 +152,17 @@ int32_t hk_hankel_rect_matvec(int64_t m, int64_t n, int32_t P,
                               uint64_t *y_mag, int8_t *y_sign,
                               void *ws, size_t ws_bytes, void *stream);
 
+/* F4: the same product (any kind; m < n allowed for HK_HANKEL as in
+ * hk_hankel_rect_matvec) with y rounded back to the input format: y_i = m_i 2^-P with
+ * m_i = round_half_even(Y_i / 2^P) (Y_i the exact integer of hk_hankel_matvec, so y_i is the exact
+ * product rounded to P fractional bits, ties to even), |m_i| < n 2^P.  y_mag[m][L+1], y_sign[m]
+ * (canonical: sign 0 iff m_i = 0).  Workspace and errors as for the exact calls.  DEVICE pointers. */
+int32_t hk_matvec_rounded(int32_t kind, int64_t m, int64_t n, int32_t P,
+                          const uint64_t *a_mag, const int8_t *a_sign,
+                          const uint64_t *x_mag, const int8_t *x_sign,
+                          uint64_t *y_mag, int8_t *y_sign,
+                          void *ws, size_t ws_bytes, void *stream);
+
 /* End-to-end call with HOST buffers (same shapes as the kind's device call; for HK_HANKEL, m may
  * be < n as in hk_hankel_rect_matvec).  Enqueues on `stream`: H2D copies of a and x into the
  * workspace's staging area, the matvec, and D2H copies of y; then synchronises `stream` and

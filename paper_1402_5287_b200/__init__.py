@@ -84,6 +84,7 @@ def _load():
                                    vp, sz, vp]),
         "hk_karatsuba_workspace_size": (i32, [i64, i32, i32, ctypes.POINTER(sz)]),
         "hk_prepare_a": (i32, [i32, i64, i64, i32, vp, vp, vp, sz, vp]),
+        "hk_matvec_rounded": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_shard_plan": (i32, [i32, i64, i32, i32, ctypes.POINTER(ShardInfo)]),
         "hk_shard_workspace_init": (i32, [i32, i64, i32, i32, vp, sz, vp]),
         "hk_hankel_shard_forward": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -104,7 +105,8 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_circulant_matvec", "hk_hankel_rect_matvec", "hk_matvec_host", "hk_matvec_host_async",
             "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
             "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared", "hk_shard_plan",
-            "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish")
+            "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish",
+            "hk_matvec_rounded")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -192,12 +194,12 @@ def _mag_dtypes():
 
 
 def _run(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None,
-         check=True):
+         check=True, rounded=False):
     import torch
     n = int(x_mag.shape[0])
     m = n if m is None else int(m)
     L = limbs(P)
-    Ly = out_limbs(P)
+    Ly = L + 1 if rounded else out_limbs(P)
     na = (n if kind == CIRCULANT else m + n - 1)
     args = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
             _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
@@ -213,7 +215,9 @@ def _run(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, strea
     if (ws.kind, ws.m, ws.n, ws.P) != (kind, m, n, P):
         raise ValueError("workspace was initialised for a different problem")
     sp = _stream_ptr(stream)
-    if kind == HANKEL and m != n:
+    if rounded:
+        rc = _lib.hk_matvec_rounded(kind, m, n, P, *args, ws.ptr, ws.nbytes, sp)
+    elif kind == HANKEL and m != n:
         rc = _lib.hk_hankel_rect_matvec(m, n, P, *args, ws.ptr, ws.nbytes, sp)
     else:
         fn = {HANKEL: _lib.hk_hankel_matvec, TOEPLITZ: _lib.hk_toeplitz_matvec,
@@ -247,8 +251,12 @@ def hankel_rect_matvec(a_mag, a_sign, x_mag, x_sign, P, m, out=None, ws=None, st
                 check=check)
 
 
-def matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None, check=True):
-    return _run(kind, a_mag, a_sign, x_mag, x_sign, P, m=m, out=out, ws=ws, stream=stream, check=check)
+def matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None, check=True,
+           rounded=False):
+    """y = A x exactly (Ly = 2L+1 limbs, scale 2^-2P), or with ``rounded`` (F4, hk_matvec_rounded)
+    rounded half-to-even back to the input format (L+1 limbs, scale 2^-P)."""
+    return _run(kind, a_mag, a_sign, x_mag, x_sign, P, m=m, out=out, ws=ws, stream=stream, check=check,
+                rounded=rounded)
 
 
 def matvec_host(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None, stream=None):

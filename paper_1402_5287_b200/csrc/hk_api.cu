@@ -260,14 +260,14 @@ bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
 int run_matvec(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
                uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream,
-               uint32_t stages = HK_STAGE_ALL) {
+               uint32_t stages = HK_STAGE_ALL, bool rounded = false) {
     if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws) return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, 0, &pl);
     if (rc) return rc;
     if (((uintptr_t)ws & 255) != 0) return HK_EINVAL;
     if (ws_bytes < pl.info.ws_bytes) return HK_ENOMEM;
-    const size_t L = pl.info.L, Ly = pl.info.Ly;
+    const size_t L = pl.info.L, Ly = rounded ? pl.info.L + 1 : pl.info.Ly;
     const size_t ya = (size_t)m * Ly * 8, ys = (size_t)m;
     const size_t aa = (size_t)pl.info.a_count * L * 8, as = (size_t)pl.info.a_count;
     const size_t xa = (size_t)n * L * 8, xs = (size_t)n;
@@ -280,6 +280,7 @@ int run_matvec(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_
     fill_params(pl, ws, &prm);
     prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
     prm.y_mag = y_mag; prm.y_sign = y_sign;
+    prm.round_out = rounded ? 1 : 0;
     if ((stages & HK_STAGE_SLICE_ROWS) &&
         cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
         return HK_ECUDA;
@@ -375,6 +376,13 @@ int32_t hk_circulant_matvec(int64_t n, int32_t P, const uint64_t *c_mag, const i
                             int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
     return run_matvec(HK_CIRCULANT, n, n, P, c_mag, c_sign, x_mag, x_sign, y_mag, y_sign, ws,
                       ws_bytes, stream);
+}
+
+int32_t hk_matvec_rounded(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
+                          const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
+                          uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    return run_matvec(kind, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws, ws_bytes,
+                      stream, HK_STAGE_ALL, true);
 }
 
 int32_t hk_hankel_rect_matvec(int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,

@@ -60,6 +60,7 @@ struct Params {
     int64_t shard_rpr;           // rows per rank block (multiple of 4); 0: not sharded
     int64_t shard_row0;          // K3: first internal row of this rank's block (g * rpr)
     int64_t y_rows;              // rows of the y buffer (m, or G * rpr when sharded)
+    int32_t round_out;           // F4: y = round_half_even(Y / 2^P) in L + 1 limbs (2^-P scale)
     // inputs / outputs (device)
     const uint64_t *a_mag;
     const int8_t *a_sign;

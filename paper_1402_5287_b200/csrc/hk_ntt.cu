@@ -422,6 +422,44 @@ HK_DEV int k3_coef_of_limb(int qq, int w, int *sh) {
     return b < 64 ? 64 * a + b : -1;
 }
 
+// F4: y rounded to the input format, m = round_half_even(|Y| / 2^P) with the sign
+// of Y (y = m 2^-P; canonical: sign 0 iff m = 0), Lr = L + 1 output limbs (|Y| / 2^P < n 2^P).
+// M: |Y| in Ly limbs (shared).  Block-wide: sticky bits, the first q limb that is not all ones
+// (where a rounding increment stops), and whether q is nonzero.
+HK_DEV void k3_store_rounded(const Params &prm, const uint64_t *M, bool neg, int64_t orow) {
+    __shared__ int s_first;
+    const int tid = threadIdx.x, T = blockDim.x, Ly = prm.Ly, Lr = prm.L + 1, P = prm.P;
+    const int qs = P >> 6, qb = P & 63, hl = (P - 1) >> 6, hb = (P - 1) & 63;
+    if (tid == 0) s_first = INT_MAX;
+    __syncthreads();
+    int sticky = 0, nz = 0;
+    for (int l = tid; l <= hl; l += T) {  // bits [0, P - 1)
+        const uint64_t v = M[l];
+        sticky |= (l < hl ? v : (v & ((1ull << hb) - 1))) != 0;
+    }
+    for (int j = tid; j < Lr; j += T) {
+        const uint64_t lo = qs + j < Ly ? M[qs + j] : 0, hi = qs + j + 1 < Ly ? M[qs + j + 1] : 0;
+        const uint64_t q = qb ? ((lo >> qb) | (hi << (64 - qb))) : lo;
+        nz |= q != 0;
+        if (q != ~0ull) atomicMin(&s_first, j);
+    }
+    sticky = __syncthreads_or(sticky);
+    nz = __syncthreads_or(nz);
+    const bool half = (M[hl] >> hb) & 1;
+    const bool lsb = (M[qs] >> qb) & 1;
+    const bool inc = half && (sticky || lsb);
+    const int first = s_first;
+    uint64_t *yo = prm.y_mag + orow * Lr;
+    for (int j = tid; j < Lr; j += T) {
+        const uint64_t lo = qs + j < Ly ? M[qs + j] : 0, hi = qs + j + 1 < Ly ? M[qs + j + 1] : 0;
+        uint64_t q = qb ? ((lo >> qb) | (hi << (64 - qb))) : lo;
+        if (inc) q = j < first ? 0ull : (j == first ? q + 1 : q);
+        yo[j] = q;
+    }
+    if (tid == 0) prm.y_sign[orow] = (nz || inc) ? (neg ? (int8_t)-1 : (int8_t)1) : (int8_t)0;
+    __syncthreads();  // s_first reuse
+}
+
 template <int LOGN2, int CH>  // CH = limbs per thread = ceil(Ly / (kK3Block / R))
 __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
     using LY = K3Layout<LOGN2>;
@@ -603,10 +641,14 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
         const int64_t orow_r = r0 + rr;
         if (orow_r >= m) break;
         const int64_t orow = prm.reverse_out ? (prm.y_rows - 1 - orow_r) : orow_r;
-        uint64_t *yo = prm.y_mag + orow * Ly;
-        for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
-        if (tid == 0)
-            prm.y_sign[orow] = s_neg[rr] ? (int8_t)-1 : (s_zmin[rr] < Ly ? (int8_t)1 : (int8_t)0);
+        if (!prm.round_out) {
+            uint64_t *yo = prm.y_mag + orow * Ly;
+            for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
+            if (tid == 0)
+                prm.y_sign[orow] = s_neg[rr] ? (int8_t)-1 : (s_zmin[rr] < Ly ? (int8_t)1 : (int8_t)0);
+        } else {
+            k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0, orow);
+        }
     }
     (void)row;
 }

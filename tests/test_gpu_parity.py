@@ -341,3 +341,46 @@ def test_prepared_requires_prepare(hk):
     rc = hk._lib.hk_matvec_prepared(0, n, n, P, x.data_ptr(), sx.data_ptr(), y.data_ptr(),
                                     ysg.data_ptr(), ws.ptr, ws.nbytes, s)
     assert rc == hk.HK_OK and ws.status() == hk.HK_EINVAL
+
+
+# ---------------------------------------------------------------------------------------------
+# F4: y rounded back to the input format (hk_matvec_rounded) vs the oracle's exact y rounded
+# by oracle/rounding.py (round half to even, pinned to round(Fraction) in test_oracle_pins.py)
+def run_gpu_rounded(hk, kind, am, asg, xm, xsg, P, m=None):
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    ym, ys = hk.matvec(kind, a, sa, x, sx, P, m=m, rounded=True)
+    torch.cuda.synchronize()
+    return hk.to_host(ym, ys)
+
+
+@pytest.mark.parametrize("kind,n,P,recipe", [
+    (0, 64, 3328, "uniform"), (1, 33, 1000, "uniform"), (2, 128, 700, "uniform"),
+    (2, 77, 2000, "carry_stress"), (0, 300, 5000, "carry_stress"), (0, 1, 64, "uniform"),
+    (1, 17, 65, "carry_stress"), (0, 129, 33216, "uniform")])
+def test_rounded_output(hk, kind, n, P, recipe):
+    from oracle import rounding as rd
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=60 + n, recipe=recipe)
+    got = run_gpu_rounded(hk, kind, am, asg, xm, xsg, P)
+    want = rd.round_rows(*oracle.matvec(kind, P, am, asg, xm, xsg), P)
+    assert_same(got, want, "rounded")
+
+
+@pytest.mark.parametrize("P", [1, 63, 64, 65, 130])
+def test_rounded_output_exact_ties(hk, P):
+    """Hankel rows whose exact value is k + 1/2 in units of 2^-P (ties go to the even k), plus
+    exact integers and a canonical zero."""
+    from oracle import rounding as rd
+    n, L = 4, (P + 63) // 64
+    half = 1 << (P - 1)
+    a_vals = [-1, 0, 0, 1, 1, 1, 0]          # a_1 .. a_7 (|a| < 2^P for every P >= 1)
+    x_vals = [half, half, half, 0]           # Y_i = (a_i + a_i+1 + a_i+2) 2^(P-1)
+    to = lambda vals: (np.array([rd.int_to_limbs(abs(v), L) for v in vals], dtype=np.uint64),
+                       np.array([(v > 0) - (v < 0) for v in vals], dtype=np.int8))
+    am, asg = to(a_vals)
+    xm, xsg = to(x_vals)
+    got = run_gpu_rounded(hk, 0, am, asg, xm, xsg, P)
+    want = rd.round_rows(*oracle.matvec(0, P, am, asg, xm, xsg), P)
+    assert_same(got, want, "rounded ties")
+    # -1/2 -> 0 (canonical zero), 1/2 -> 0, exactly 1, 3/2 -> 2
+    assert [int(v) for v in got[0][:, 0]] == [0, 0, 1, 2] and list(got[1]) == [0, 0, 1, 1]

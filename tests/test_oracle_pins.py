@@ -234,3 +234,32 @@ def test_carry_stress_config_rows_vs_bruteforce():
         ym, ys = oracle.matvec(kind, 1000, am, asg, xm, xsg, threads=2)
         bm, bs = bf.matvec(kind, 1000, am, asg, xm, xsg)
         assert np.array_equal(ym, bm) and np.array_equal(ys, bs)
+
+
+# ---------------------------------------------------------------------------------------------
+# F4 rounding (oracle/rounding.py): pinned to Python's round(Fraction), which rounds half to even
+def test_round_half_even_matches_fraction_round():
+    import random
+    from fractions import Fraction
+    from oracle import rounding as rd
+    rng = random.Random(7)
+    for P in (1, 2, 5, 63, 64, 65, 127, 128, 200):
+        for _ in range(200):
+            Y = rng.getrandbits(2 * P + 14) * rng.choice((-1, 1))
+            assert rd.round_half_even_int(Y, P) == round(Fraction(Y, 1 << P))
+        for k in (-5, -3, -1, 0, 1, 2, 3, 4):  # exact ties k + 1/2 and exact integers
+            Yt = (2 * k + 1) << (P - 1)
+            assert rd.round_half_even_int(Yt, P) == round(Fraction(Yt, 1 << P))
+            assert rd.round_half_even_int(k << P, P) == k
+
+
+def test_round_half_even_closed_cases():
+    from oracle import rounding as rd
+    assert [rd.round_half_even_int(Y, 1) for Y in (1, 3, 5, 7, -1, -3, -5)] == [0, 2, 2, 4, 0, -2, -2]
+    P = 70  # increment carrying across limbs: (2^128 - 1) + 1/2 + tiny -> 2^128
+    Y = ((1 << 128) - 1 << P) + (1 << (P - 1)) + 1
+    assert rd.round_half_even_int(Y, P) == 1 << 128
+    m, s = rd.round_rows(np.array([rd.int_to_limbs(Y, 5)], dtype=np.uint64), np.array([1], np.int8), 128)
+    assert s[0] == 1 and rd.limbs_to_int(m[0]) == rd.round_half_even_int(Y, 128)
+    m, s = rd.round_rows(np.array([[1, 0, 0]], dtype=np.uint64), np.array([-1], np.int8), 64)
+    assert s[0] == 0 and not m.any()  # -2^-128 rounds to a canonical zero

@@ -524,6 +524,33 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
     const int r = tid % R, k = tid / R, lane_r = lane / R;  // lane_r: position among the row's lanes
     const int64_t row = r0 + r;
     const int l0 = k * CH;
+    // Sliding window over consecutive limbs: W[d] holds the shifted words S_0..S_3 and the sign of
+    // the coefficient at limb index q = l - d, so every coefficient is read and shifted once.
+    struct ShiftedCoef { uint64_t s0, s1, s2, s3; uint32_t neg; };
+    auto load_coef = [&](int qq) -> ShiftedCoef {
+        ShiftedCoef z = {0, 0, 0, 0, 0};
+        if (qq < 0) return z;
+        int sh;
+        const int sidx = k3_coef_of_limb(qq, w, &sh);
+        if (sidx < 0 || sidx >= S2) return z;
+        const uint64_t C0 = (uint64_t)sm[LY::idx(0, sidx, r)] | ((uint64_t)sm[LY::idx(1, sidx, r)] << 32);
+        const uint64_t C1 = (uint64_t)sm[LY::idx(2, sidx, r)] | ((uint64_t)sm[LY::idx(3, sidx, r)] << 32);
+        const uint32_t w4 = sm[LY::idx(4, sidx, r)];
+        const uint64_t C2 = (uint64_t)(int64_t)(int32_t)w4;   // sign-extended bits 128..159
+        const uint64_t C3 = (uint64_t)((int64_t)C2 >> 63);      // sign word
+        if (sh) {
+            z.s0 = C0 << sh;
+            z.s1 = (C1 << sh) | (C0 >> (64 - sh));
+            z.s2 = (C2 << sh) | (C1 >> (64 - sh));
+            z.s3 = (C3 << sh) | (C2 >> (64 - sh));
+        } else {
+            z.s0 = C0; z.s1 = C1; z.s2 = C2; z.s3 = C3;
+        }
+        z.neg = (uint32_t)(C3 & 1u);  // -1 at limb q + 4 (sign extension beyond S_3)
+        return z;
+    };
+    ShiftedCoef W1 = load_coef(l0 - 1), W2 = load_coef(l0 - 2), W3 = load_coef(l0 - 3),
+                W4 = load_coef(l0 - 4);
     uint64_t u[CH];
     int e[CH];
 #pragma unroll
@@ -532,40 +559,14 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
         uint64_t acc = 0;
         int hi = 0;
         if (l < Ly) {
-#pragma unroll
-            for (int d = 0; d < 5; ++d) {  // word d of coefficient s with q(s) = l - d; d = 4: sign borrow
-                const int qq = l - d;
-                if (qq < 0) break;
-                int sh;
-                const int s = k3_coef_of_limb(qq, w, &sh);
-                if (s < 0 || s >= S2) continue;
-                const uint32_t w4 = sm[LY::idx(4, s, r)];
-                const uint64_t C3 = (uint64_t)((int64_t)(int32_t)w4 >> 31);  // sign word
-                if (d == 4) {  // -1 at limb q + 4 when C_s < 0 (sign extension beyond S_3)
-                    const uint64_t bw = C3 & 1u;
-                    hi -= (int)(bw & (acc == 0));
-                    acc -= bw;
-                    continue;
-                }
-                const uint64_t C2 = (uint64_t)(int64_t)(int32_t)w4;
-                uint64_t cd, cm;  // C_d and C_{d-1}
-                if (d == 0) {
-                    cd = (uint64_t)sm[LY::idx(0, s, r)] | ((uint64_t)sm[LY::idx(1, s, r)] << 32);
-                    cm = 0;
-                } else if (d == 1) {
-                    cd = (uint64_t)sm[LY::idx(2, s, r)] | ((uint64_t)sm[LY::idx(3, s, r)] << 32);
-                    cm = (uint64_t)sm[LY::idx(0, s, r)] | ((uint64_t)sm[LY::idx(1, s, r)] << 32);
-                } else if (d == 2) {
-                    cd = C2;
-                    cm = (uint64_t)sm[LY::idx(2, s, r)] | ((uint64_t)sm[LY::idx(3, s, r)] << 32);
-                } else {
-                    cd = C3;
-                    cm = C2;
-                }
-                const uint64_t word = sh ? ((cd << sh) | (cm >> (64 - sh))) : cd;
-                acc += word;
-                hi += acc < word;
-            }
+            const ShiftedCoef W0 = load_coef(l);
+            acc = W0.s0;
+            acc += W1.s1; hi += acc < W1.s1;
+            acc += W2.s2; hi += acc < W2.s2;
+            acc += W3.s3; hi += acc < W3.s3;
+            hi -= (int)(W4.neg & (acc == 0));
+            acc -= W4.neg;
+            W4 = W3; W3 = W2; W2 = W1; W1 = W0;
         }
         u[c] = acc;
         e[c] = hi;  // carry into limb l + 1, in [-1, 3]

@@ -161,6 +161,14 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     off = align256(off + (size_t)kNumPrimes * N2loc * pl->ldX * 4);
     pl->off_Y = off;  // sharded: K2 writes the caller's all-to-all send buffer instead
     if (G == 1) off = align256(off + (size_t)kNumPrimes * N2 * pl->ldY * 4);
+    // N1 >= 2^15: K2 runs as two launches (A^'s column transform to AT, then X^'s transform x AT
+    // + inverse), since one thread cannot hold N1 / 512 = 64 X^ values beside its working set
+    const size_t at_bytes = (size_t)kNumPrimes * N2loc * N1 * 4;
+    pl->split_k2 = in.log_n1 >= kSplitLogN1;
+    if (pl->split_k2) {
+        pl->off_AT = off;
+        off = align256(off + at_bytes);
+    }
     pl->off_end = off;
     pl->off_stage = off;
     const size_t L = in.L, Ly = in.Ly;
@@ -171,9 +179,10 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     pl->st_ymag = off;  off = align256(off + (size_t)m * Ly * 8);
     pl->st_ysign = off; off = align256(off + (size_t)m);
     pl->off_end_staging = off;
-    // HK_WS_PREPARED: the 2-D transform of a right after the base layout
-    pl->off_AT = pl->off_end;
-    pl->off_end_prepared = align256(pl->off_AT + (size_t)kNumPrimes * N2 * N1 * 4);
+    // HK_WS_PREPARED: the 2-D transform of a right after the base layout (already inside it when
+    // K2 is split)
+    if (!pl->split_k2) pl->off_AT = pl->off_end;
+    pl->off_end_prepared = pl->split_k2 ? pl->off_end : align256(pl->off_AT + at_bytes);
     in.ws_bytes = pl->off_end;
     in.ws_bytes_staging = pl->off_end_staging;
     in.ws_bytes_prepared = pl->off_end_prepared;
@@ -215,6 +224,8 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
     prm->tw = (const uint2 *)(base + pl.off_tw);
     prm->Ahat = (uint32_t *)(base + pl.off_A);
     prm->Xhat = (uint32_t *)(base + pl.off_X);
+    prm->AT = pl.split_k2 ? (uint32_t *)(base + pl.off_AT) : nullptr;
+    prm->split_k2 = pl.split_k2;
     prm->Yhat = (uint32_t *)(base + pl.off_Y);
     const uint64_t N12 = (uint64_t)prm->N1 * (uint64_t)prm->N2;
     for (int k = 0; k < kNumPrimes; ++k) {

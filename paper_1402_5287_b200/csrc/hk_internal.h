@@ -12,6 +12,7 @@ constexpr int kNumPrimes = 5;
 constexpr uint64_t kWsMagic = 0x484b5753504c414eull;  // "HKWSPLAN"
 constexpr int kMaxLogN1 = 15;                           // N1 <= 32768 (K2 register budget)
 constexpr int kMinLogN1 = 6;
+constexpr int kSplitLogN1 = 15;                         // K2 as prepare + prepared launches from here
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
@@ -75,6 +76,7 @@ struct Params {
                                    // buffer when sharded)
     uint32_t *AT;                // prepared 2-D transform of a (HK_WS_PREPARED), or null
     int32_t need_a_ready;        // K1 (x tiles): require hdr->a_ready
+    int32_t split_k2;            // K2 as MODE 1 (A^ -> AT) + MODE 2 (X^ x AT, inverse) launches
     PrimeConsts pc[kNumPrimes];
     GarnerConsts gc;
 };
@@ -89,6 +91,7 @@ struct Plan {
     size_t off_tw, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
     size_t st_amag, st_asign, st_xmag, st_xsign, st_ymag, st_ysign;
     size_t off_AT, off_end_prepared;
+    int32_t split_k2;            // N1 >= 2^kSplitLogN1: AT inside the base layout, K2 in two launches
 };
 
 // kernels (hk_ntt.cu)

@@ -303,7 +303,7 @@ HK_DEV void k2_prepare_body(const Params &prm, uint32_t *sm, const uint2 *twf, i
 }
 
 // F1 prepared matvec: X^ forward, pointwise with the stored A^ transform, inverse.
-template <class TW, int LOGN1>
+template <class TW, int LOGN1, bool SHARD = false>
 HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
     using PL = ColPlan<LOGN1>;
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
@@ -330,12 +330,13 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
         for (int m = 0; m < GL; ++m) sm[pad(g * GL + m)] = v[m];
     }
     __syncthreads();
-    k2_inverse_tail<TW, LOGN1>(prm, sm, twf, p, cidx);
+    k2_inverse_tail<TW, LOGN1, SHARD>(prm, sm, twf, p, cidx);
 }
 
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
 // MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT);
-// 3: full column of a sigma-coset shard (output to the all-to-all send buffer).
+// 3: full column of a sigma-coset shard (output to the all-to-all send buffer); 4: prepared column
+// of a shard.  N1 >= 2^15 runs MODE 1 then MODE 2 (4 for shards) instead of MODE 0 (3).
 template <int LOGN1, class TW = TwGlobal, int MODE = 0>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k
     if constexpr (MODE == 0) k2_column_body<TW, LOGN1, false>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 3) k2_column_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 1) k2_prepare_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
-    else k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
+    else if constexpr (MODE == 2) k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
+    else k2_prepared_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);
 }
 
 }  // namespace hk

@@ -715,9 +715,21 @@ static int launch_cols_m(const Params &prm, cudaStream_t st) {
     k2_column<LOGN1, TwGlobal, MODE><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
 }
+template <int LOGN1, int MODE>
+static int launch_cols_mode(const Params &prm, cudaStream_t st);
+
 template <int LOGN1>
 static int launch_cols(const Params &prm, cudaStream_t st) {
-    return prm.shard_rpr ? launch_cols_m<LOGN1, 3>(prm, st) : launch_cols_m<LOGN1, 0>(prm, st);
+    if constexpr (LOGN1 >= kSplitLogN1) {  // A^ transform -> AT, then X^ transform x AT + inverse
+        if (!prm.split_k2 || !prm.AT) return HK_EINVAL;
+        // AT now holds this call's A^: a prepared matrix kept in this workspace is gone
+        if (cudaMemsetAsync(&prm.hdr->a_ready, 0, sizeof(int32_t), st) != cudaSuccess) return HK_ECUDA;
+        int rc = launch_cols_mode<LOGN1, 1>(prm, st);
+        if (rc) return rc;
+        return prm.shard_rpr ? launch_cols_mode<LOGN1, 4>(prm, st) : launch_cols_mode<LOGN1, 2>(prm, st);
+    } else {
+        return prm.shard_rpr ? launch_cols_m<LOGN1, 3>(prm, st) : launch_cols_m<LOGN1, 0>(prm, st);
+    }
 }
 
 int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {

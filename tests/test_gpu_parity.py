@@ -384,3 +384,21 @@ def test_rounded_output_exact_ties(hk, P):
     assert_same(got, want, "rounded ties")
     # -1/2 -> 0 (canonical zero), 1/2 -> 0, exactly 1, 3/2 -> 2
     assert [int(v) for v in got[0][:, 0]] == [0, 0, 1, 2] and list(got[1]) == [0, 0, 1, 1]
+
+
+def test_split_k2_large_n1(hk):
+    """N1 = 2^15 (n > 8192) runs K2 as prepare + prepared launches through the workspace's AT
+    region: bit-exact (all rows, small P), a prepared matrix in the same workspace serves
+    vectors, and a cold call on that workspace invalidates it (AT overwritten)."""
+    n, P = 8200, 64
+    assert hk.plan(0, n, P)["log_n1"] == 15
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=77)
+    got = run_gpu(hk, 0, am, asg, xm, xsg, P)
+    assert_same(got, oracle.matvec(0, P, am, asg, xm, xsg), "split K2")
+    A = hk.PreparedMatrix(0, *hk.to_device(am, asg), P, n)
+    x2m, x2s = gen.uniform(9, 1, n, P)
+    assert_same(hk.to_host(*A.matvec(*hk.to_device(x2m, x2s))),
+                oracle.matvec(0, P, am, asg, x2m, x2s), "split K2 prepared")
+    hk.matvec(0, *hk.to_device(am, asg), *hk.to_device(xm, xsg), P, ws=A.ws)  # cold call, same ws
+    with pytest.raises(hk.HKError):
+        A.matvec(*hk.to_device(x2m, x2s))

@@ -68,8 +68,9 @@ HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, b
                 gs_bfly(v[m], v[m + half], w, p);
             }
         }
+        uint32_t *b0 = sm + pad(j0);  // pad(j0 + m S) = pad(j0) + pad(m S) (S multiple of 32)
 #pragma unroll
-        for (int m = 0; m < G; ++m) sm[pad(j0 + m * S)] = v[m];
+        for (int m = 0; m < G; ++m) b0[padded_len(m * S)] = v[m];
     }
     __syncthreads();
 }
@@ -145,8 +146,9 @@ HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, const Params &
     constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
     for (int j0 = threadIdx.x; j0 < S; j0 += T) {
         uint32_t v[G];
+        uint32_t *b0 = sm + pad(j0);  // S multiple of 32
 #pragma unroll
-        for (int m = 0; m < G; ++m) v[m] = sm[pad(j0 + m * S)];
+        for (int m = 0; m < G; ++m) v[m] = b0[padded_len(m * S)];
 #pragma unroll
         for (int l = 0; l < R; ++l) {
             const int half = 1 << l;
@@ -159,7 +161,7 @@ HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, const Params &
         }
         if (to_smem) {
 #pragma unroll
-            for (int m = 0; m < G; ++m) sm[pad(j0 + m * S)] = v[m];
+            for (int m = 0; m < G; ++m) b0[padded_len(m * S)] = v[m];
         } else {
 #pragma unroll
             for (int m = 0; m < G; ++m) {
@@ -210,7 +212,7 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     for (int k = 0; k < GPT; ++k) {
         const int g = tid + k * T;
 #pragma unroll
-        for (int m = 0; m < GL; ++m) xr[k][m] = sm[pad(g * GL + m)];
+        for (int m = 0; m < GL; ++m) xr[k][m] = sm[pad(g * GL) + m];
         dif_bottom_regs<TW, RL>(xr[k], twf, p);
     }
     __syncthreads();
@@ -232,13 +234,13 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         const int g = tid + k * T;
         uint32_t v[GL];
 #pragma unroll
-        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL + m)];
+        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL) + m];
         dif_bottom_regs<TW, RL>(v, twf, p);
 #pragma unroll
         for (int m = 0; m < GL; ++m) v[m] = mont(v[m], xr[k][m], p, pneg);
         dit_bottom_regs<TW, RL>(v, twf, p);
 #pragma unroll
-        for (int m = 0; m < GL; ++m) sm[pad(g * GL + m)] = v[m];
+        for (int m = 0; m < GL; ++m) sm[pad(g * GL) + m] = v[m];
     }
     __syncthreads();
     K2DitMiddle<TW, LOGN1, RL>::run(sm, twf, p);
@@ -295,7 +297,7 @@ HK_DEV void k2_prepare_body(const Params &prm, uint32_t *sm, const uint2 *twf, i
         const int g = tid + k * T;
         uint32_t v[GL];
 #pragma unroll
-        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL + m)];
+        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL) + m];
         dif_bottom_regs<TW, RL>(v, twf, p);
 #pragma unroll
         for (int m = 0; m < GL; ++m) at[(k * GL + m) * T + tid] = v[m];
@@ -321,13 +323,13 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
 #pragma unroll
         for (int m = 0; m < GL; ++m) av[m] = __ldcs(at + (k * GL + m) * T + tid);
 #pragma unroll
-        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL + m)];
+        for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL) + m];
         dif_bottom_regs<TW, RL>(v, twf, p);
 #pragma unroll
         for (int m = 0; m < GL; ++m) v[m] = mont(av[m], v[m], p, pneg);
         dit_bottom_regs<TW, RL>(v, twf, p);
 #pragma unroll
-        for (int m = 0; m < GL; ++m) sm[pad(g * GL + m)] = v[m];
+        for (int m = 0; m < GL; ++m) sm[pad(g * GL) + m] = v[m];
     }
     __syncthreads();
     k2_inverse_tail<TW, LOGN1, SHARD>(prm, sm, twf, p, cidx);

@@ -123,12 +123,14 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
         const unsigned g = gi % NG;
         const unsigned j0 = g % S;
         const unsigned B = (g / S) * (S * G);
-        uint32_t *base = s + b * rs;
+        // pad(B + j0 + m S) = pad(B + j0) + pad(m S): B is a multiple of S G and S G | 32 or 32 | S G,
+        // so the low part never carries into bit 5 -- the per-point offset is an immediate
+        uint32_t *base = s + b * rs + padu(B + j0);
         uint32_t v[G];
 #pragma unroll
         for (int m = 0; m < G; ++m) {
             if (ZERO_UPPER && m >= G / 2) v[m] = 0;
-            else v[m] = base[padu(B + j0 + m * S)];
+            else v[m] = base[padded_len(m * S)];
         }
 #pragma unroll
         for (int l = R - 1; l >= 0; --l) {
@@ -146,7 +148,7 @@ HK_DEV void dif_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) base[padu(B + j0 + m * S)] = v[m];
+        for (int m = 0; m < G; ++m) base[padded_len(m * S)] = v[m];
     }
     __syncthreads();
 }
@@ -164,10 +166,10 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
         const unsigned g = gi % NG;
         const unsigned j0 = g % S;
         const unsigned B = (g / S) * (S * G);
-        uint32_t *base = s + b * rs;
+        uint32_t *base = s + b * rs + padu(B + j0);  // see dif_pass
         uint32_t v[G];
 #pragma unroll
-        for (int m = 0; m < G; ++m) v[m] = base[padu(B + j0 + m * S)];
+        for (int m = 0; m < G; ++m) v[m] = base[padded_len(m * S)];
 #pragma unroll
         for (int l = 0; l < R; ++l) {
             const int half = 1 << l;
@@ -184,7 +186,7 @@ HK_DEV void dit_pass(uint32_t *s, int batch, int rs, const uint2 *__restrict__ t
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) base[padu(B + j0 + m * S)] = v[m];
+        for (int m = 0; m < G; ++m) base[padded_len(m * S)] = v[m];
     }
     __syncthreads();
 }

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
                 }
             }
 #pragma unroll
-            for (int m = 0; m < GK; ++m) sm[r * RS + pad(j0 + m * S1)] = v[m];
+            for (int m = 0; m < GK; ++m) sm[r * RS + pad(j0) + padded_len(m * S1)] = v[m];
         }
         __syncthreads();
         constexpr int REM = LOGN2 - R1;          // stages left after the top pass
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
             const int rr = gi % kK1Rows, g = gi / kK1Rows;
             uint32_t v[GB];
 #pragma unroll
-            for (int m = 0; m < GB; ++m) v[m] = sm[rr * RS + pad(g * GB + m)];
+            for (int m = 0; m < GB; ++m) v[m] = sm[rr * RS + pad(g * GB) + m];
             dif_bottom_regs<TwShared, RB>(v, tw, p);
             const int64_t orow = r0 + rr;
             if (orow < count) {

@@ -148,10 +148,12 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     pl->rpr = G == 1 ? 0 : ((m + G - 1) / G + 3) / 4 * 4;
     const int64_t N2 = int64_t(1) << in.log_n2;
     const int64_t N2loc = N2 / G;
-    pl->ldA = (in.a_count + 31) / 32 * 32;
-    pl->ldX = (n + 31) / 32 * 32;
-    pl->ldY = (m + 31) / 32 * 32;
     const int64_t N1 = int64_t(1) << in.log_n1;
+    // A^ / X^ columns: zero-padded up to the extent K2's top pass loads (N1 / 2 when the count fits
+    // in the lower half, else N1); K1 writes rows < count only and hk_workspace_init zeroes the rest
+    pl->ldA = in.a_count <= N1 / 2 ? N1 / 2 : N1;
+    pl->ldX = n <= N1 / 2 ? N1 / 2 : N1;
+    pl->ldY = (m + 31) / 32 * 32;
     size_t off = align256(sizeof(WsHeader));
     pl->off_tw = off;
     off = align256(off + (size_t)kNumPrimes * (N1 + N2) * sizeof(uint2));
@@ -263,6 +265,16 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
         }
 }
 
+// Twiddle tables + header (K0), and zeros in the A^ / X^ arrays: their column padding beyond the
+// entry count is never written by K1 and must read as zero in K2 (see ldA / ldX in make_plan).
+int init_workspace(const Plan &pl, const Params &prm, void *ws, void *stream) {
+    if (cudaMemsetAsync((char *)ws + pl.off_A, 0, pl.off_Y - pl.off_A, (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    uint32_t gens[kNumPrimes];
+    for (int k = 0; k < kNumPrimes; ++k) gens[k] = primitive_root(kPrimesHost[k]);
+    return launch_init(prm, gens, stream);
+}
+
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
     const char *pa = (const char *)a, *pb = (const char *)b;
     return pa < pb + nb && pb < pa + na;
@@ -351,9 +363,7 @@ int32_t hk_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_
     if (ws_bytes < need) return HK_ENOMEM;
     Params prm;
     fill_params(pl, ws, &prm);
-    uint32_t gens[kNumPrimes];
-    for (int k = 0; k < kNumPrimes; ++k) gens[k] = primitive_root(kPrimesHost[k]);
-    return launch_init(prm, gens, stream);
+    return init_workspace(pl, prm, ws, stream);
 }
 
 int32_t hk_workspace_status(void *ws, void *stream, int32_t *data_status) {
@@ -575,9 +585,7 @@ int32_t hk_shard_workspace_init(int32_t kind, int64_t n, int32_t P, int32_t G, v
     if (ws_bytes < pl.info.ws_bytes) return HK_ENOMEM;
     Params prm;
     fill_params(pl, ws, &prm);
-    uint32_t gens[kNumPrimes];
-    for (int k = 0; k < kNumPrimes; ++k) gens[k] = primitive_root(kPrimesHost[k]);
-    return launch_init(prm, gens, stream);
+    return init_workspace(pl, prm, ws, stream);
 }
 
 static int shard_common(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g, void *ws,

@@ -45,18 +45,20 @@ struct ColPlan {
 };
 
 // Top forward pass (R = 5, S = N/32, single block) reading the column straight from HBM
-// (SRC_SMEM = false) or from a shared-memory staging copy (SRC_SMEM = true).
-template <class TW, int LOGN, int T, bool SRC_SMEM = false>
-HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, bool zu,
-                                   uint32_t *sm, const uint2 *tw, uint32_t p) {
+// (SRC_SMEM = false) or from a shared-memory staging copy (SRC_SMEM = true).  The column is zero-
+// padded in the workspace up to its loaded extent (N/2 when the upper half is known to be zero, ZU,
+// else N; hk_api.cu make_plan), so the loads need no bounds checks.
+template <class TW, int LOGN, int T, bool SRC_SMEM, bool ZU>
+HK_DEV void k2_dif_top_load(const uint32_t *__restrict__ src, uint32_t *sm, const uint2 *tw,
+                            uint32_t p) {
     constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
     for (int j0 = threadIdx.x; j0 < S; j0 += T) {
         uint32_t v[G];
 #pragma unroll
         for (int m = 0; m < G; ++m) {
-            const int idx = j0 + m * S;
-            if (SRC_SMEM) v[m] = (!(zu && m >= G / 2) && idx < nsrc) ? src[idx] : 0u;
-            else v[m] = (!(zu && m >= G / 2) && idx < nsrc) ? __ldcs(src + idx) : 0u;
+            if (ZU && m >= G / 2) v[m] = 0u;
+            else if (SRC_SMEM) v[m] = src[j0 + m * S];
+            else v[m] = __ldcs(src + j0 + m * S);
         }
 #pragma unroll
         for (int l = R - 1; l >= 0; --l) {
@@ -64,6 +66,11 @@ HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, b
 #pragma unroll
             for (int m = 0; m < G; ++m) {
                 if (m & half) continue;
+                if (ZU && l == R - 1) {  // (u, 0) -> (u, u W)
+                    const uint2 w = TW::ld(tw, S * half + j0 + S * m);
+                    v[m + half] = red1(shoup(v[m], w.x, w.y, p), p);
+                    continue;
+                }
                 const uint2 w = TW::ld(tw, S * half + j0 + S * (m & (half - 1)));
                 gs_bfly(v[m], v[m + half], w, p);
             }
@@ -73,6 +80,12 @@ HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, int nsrc, b
         for (int m = 0; m < G; ++m) b0[padded_len(m * S)] = v[m];
     }
     __syncthreads();
+}
+template <class TW, int LOGN, int T, bool SRC_SMEM = false>
+HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, bool zu, uint32_t *sm,
+                                   const uint2 *tw, uint32_t p) {
+    if (zu) k2_dif_top_load<TW, LOGN, T, SRC_SMEM, true>(src, sm, tw, p);
+    else k2_dif_top_load<TW, LOGN, T, SRC_SMEM, false>(src, sm, tw, p);
 }
 
 // Middle forward passes (R = 5), k = 1 .. NP-2.
@@ -195,8 +208,7 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     uint32_t *sA = sm + k2_stage_off<LOGN1>();
     if constexpr (STAGE) {  // issue the A^ column copy now; consumed after X^'s transform
-        const int na = (int)prm.a_count;
-        const int nch = (na < N1 ? na : N1) + 3 >> 2;
+        const int nch = (int)prm.ldA >> 2;  // the zero-padded column (ldA = N1 or N1 / 2)
         const uint32_t *g = prm.Ahat + cidx * prm.ldA;
         for (int c = tid; c < nch; c += T) cp_async16(sA + 4 * c, g + 4 * c);
     }
@@ -204,7 +216,7 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     // ---- X^: forward, bottom pass kept in registers
     {
         const int nx = (int)prm.n;
-        k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx, nx <= N1 / 2, sm, twf, p);
+        k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
         K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     }
     uint32_t xr[GPT][GL];
@@ -222,10 +234,9 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         if constexpr (STAGE) {
             cp_async_wait_all();
             __syncthreads();
-            k2_dif_top_from_global<TW, LOGN1, T, true>(sA, na, na <= N1 / 2, sm, twf, p);
+            k2_dif_top_from_global<TW, LOGN1, T, true>(sA, na <= N1 / 2, sm, twf, p);
         } else {
-            k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm,
-                                                 twf, p);
+            k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na <= N1 / 2, sm, twf, p);
         }
         K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     }
@@ -289,7 +300,7 @@ HK_DEV void k2_prepare_body(const Params &prm, uint32_t *sm, const uint2 *twf, i
     const uint32_t p = prm.pc[kp].p;
     const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     const int na = (int)prm.a_count;
-    k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na, na <= N1 / 2, sm, twf, p);
+    k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na <= N1 / 2, sm, twf, p);
     K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     uint32_t *at = prm.AT + cidx * N1;
 #pragma unroll
@@ -313,7 +324,7 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
     const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     const int nx = (int)prm.n;
-    k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx, nx <= N1 / 2, sm, twf, p);
+    k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
     K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     const uint32_t *at = prm.AT + cidx * N1;
 #pragma unroll

@@ -294,17 +294,18 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
 //   (c) per row: Y = sum_s C_s 2^(w s) mod 2^(64 Ly) gathered limb by limb (w in {64, 65}
 //       makes the limb index q(s) = floor(w s / 64) injective), carries resolved by a block
 //       scan of carry-transfer functions, two's complement -> sign-magnitude, coalesced store.
-// Shared layout: word (prime kp, slice sigma, row r) at kp * N2 * R + swz(sigma) * R + r with
-// swz(sigma) = sigma ^ ((sigma >> 5) & (32/R - 1)): rows interleaved so one 16-byte cp.async
-// brings the R rows of a (prime, sigma) column segment; the XOR keeps the strided (S >= 32/R)
-// and the contiguous (S = 1, radix 32) passes and the Garner pairs bank-conflict-free.
+// Shared layout: word (prime kp, slice sigma, row r) at kp PS + pad(sigma) R + r with
+// pad(sigma) = sigma + sigma / 32: rows interleaved so one 16-byte cp.async brings the R rows of a
+// (prime, sigma) column segment; the pad keeps the contiguous (S = 1, radix 32: lanes 32 sigma
+// apart) and the strided (S >= 32 / R) passes and the Garner pairs bank-conflict-free, and it is
+// separable (pad(B + j0 + m S) = pad(B + j0) + pad(m S)) so per-point offsets are immediates.
 template <int LOGN2>
 constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : 4; }
 
 template <int LOGN2>
 struct K3Layout {
-    static constexpr int N2 = 1 << LOGN2, R = k3_rows<LOGN2>(), OCT = 32 / R, PS = N2 * R;
-    static HK_DEV int idx(int kp, int s, int r) { return kp * PS + (s ^ ((s >> 5) & (OCT - 1))) * R + r; }
+    static constexpr int N2 = 1 << LOGN2, R = k3_rows<LOGN2>(), PS = padded_len(N2) * R;
+    static HK_DEV int idx(int kp, int s, int r) { return kp * PS + pad(s) * R + r; }
     static constexpr size_t res_words() { return (size_t)kNumPrimes * PS; }
 };
 
@@ -374,9 +375,10 @@ HK_DEV void k3_dit_pass(uint32_t *sm, const Params &prm) {
         const uint32_t p = prm.pc[kp].p;
         const uint2 *tw = prm.tw + (size_t)kp * (prm.N2 + prm.N1);
         const int j0 = g % S, B = (g / S) * (S * G);
+        uint32_t *b0 = sm + LY::idx(kp, B + j0, r);
         uint32_t v[G];
 #pragma unroll
-        for (int m = 0; m < G; ++m) v[m] = sm[LY::idx(kp, B + j0 + m * S, r)];
+        for (int m = 0; m < G; ++m) v[m] = b0[padded_len(m * S) * R];
 #pragma unroll
         for (int l = 0; l < RR; ++l) {
             const int half = 1 << l;
@@ -388,7 +390,7 @@ HK_DEV void k3_dit_pass(uint32_t *sm, const Params &prm) {
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) sm[LY::idx(kp, B + j0 + m * S, r)] = v[m];
+        for (int m = 0; m < G; ++m) b0[padded_len(m * S) * R] = v[m];
     }
     __syncthreads();
 }

@@ -478,8 +478,11 @@ def main():
                    "plan": {k: plan[k] for k in ("w", "Ls", "log_n1", "log_n2", "k_primes",
                                                  "margin_bits")},
                    "parallelism": "single GPU" if world == 1 else (
-                       f"sigma-coset x{world}: NCCL all-to-all + all-gather" if args.plan == "coset"
-                       else f"row-block x{world} + NCCL all-gather"),
+                       (f"sigma-coset x{world}: " + ("exchanges fused into K2/K3 stores over peer memory "
+                                                     "(symmetric memory, NVLink) + device barriers"
+                                                     if getattr(sh, "p2p", False) else
+                                                     "NCCL all-to-all + all-gather"))
+                       if args.plan == "coset" else f"row-block x{world} + NCCL all-gather"),
                    "l2": "no flush: per-step working set (inputs 100 MB + transform-domain "
                          f"{all_bytes / 1e6:.0f} MB traffic) exceeds the 126 MB L2"},
         "stages_ms": dict(zip(stage_names, stage_ms)),

@@ -233,6 +233,26 @@ int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, in
                                const uint32_t *recv, uint64_t *y_mag, int8_t *y_sign, void *ws,
                                size_t ws_bytes, void *stream);
 
+/* The same two phases with the collectives fused into the kernels' stores over peer memory
+ * (NVLink / NVSwitch P2P; pointers mapped into this process, e.g. torch symmetric memory):
+ *   forward_p2p: recv_ptrs[r] (host array of G device pointers) = rank r's receive buffer
+ *     (buffer_words); K2 writes this rank's chunk for destination r directly at slot g of rank
+ *     r's buffer, so no all-to-all is needed.  Every rank must have finished its forward_p2p before
+ *     any rank's finish reads its receive buffer (a device or host barrier after the kernels).
+ *   finish_p2p: recv = this rank's receive buffer; y_mag_ptrs[d] / y_sign_ptrs[d] = rank d's padded
+ *     y buffers (y_rows rows); K3 writes this rank's rows into all G of them (the all-gather fused
+ *     into its stores); a barrier after it completes the exchange.
+ * Bit-identical to the NCCL-exchange path. */
+int32_t hk_hankel_shard_forward_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                    const uint64_t *a_mag, const int8_t *a_sign,
+                                    const uint64_t *x_mag, const int8_t *x_sign,
+                                    uint32_t *const *recv_ptrs, void *ws, size_t ws_bytes,
+                                    void *stream);
+int32_t hk_hankel_shard_finish_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                   const uint32_t *recv, uint64_t *const *y_mag_ptrs,
+                                   int8_t *const *y_sign_ptrs, void *ws, size_t ws_bytes,
+                                   void *stream);
+
 /* Pipeline stages of the NTT path, for per-kernel timing (bench.py) and phase-wise use:
  *   HK_STAGE_SLICE_ROWS  K1: validation, slicing, slice-dimension forward NTT of a and x
  *   HK_STAGE_COLUMNS     K2: matrix-index forward NTTs, pointwise product, inverse NTT

@@ -89,6 +89,8 @@ def _load():
         "hk_shard_workspace_init": (i32, [i32, i64, i32, i32, vp, sz, vp]),
         "hk_hankel_shard_forward": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
         "hk_hankel_shard_finish": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_forward_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_finish_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_prepared": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     }
@@ -106,7 +108,7 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
             "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared", "hk_shard_plan",
             "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish",
-            "hk_matvec_rounded")
+            "hk_matvec_rounded", "hk_hankel_shard_forward_p2p", "hk_hankel_shard_finish_p2p")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -279,6 +281,42 @@ def matvec_host(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, ws=None
                              hptr(out[0]), hptr(out[1]), ws.ptr, ws.nbytes, _stream_ptr(stream))
     _check(rc, "hk_matvec_host")
     return out
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+    return arr
+
+
+def shard_forward_p2p(ws: ShardWorkspace, g, a_mag, a_sign, x_mag, x_sign, recv_ptrs, stream=None):
+    """Phase 1 of rank g with the all-to-all fused into K2's stores: recv_ptrs[r] = rank r's receive
+    buffer (device pointers mapped into this process, e.g. torch symmetric memory)."""
+    import torch
+    L, na = limbs(ws.P), (ws.n if ws.kind == CIRCULANT else 2 * ws.n - 1)
+    if len(recv_ptrs) != ws.G:
+        raise ValueError("need one receive-buffer pointer per rank")
+    ptrs = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (ws.n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (ws.n,), "x_sign")]
+    arr = _ptr_array(recv_ptrs)
+    _check(_lib.hk_hankel_shard_forward_p2p(ws.kind, ws.n, ws.P, ws.G, int(g), *ptrs,
+                                            ctypes.cast(arr, ctypes.c_void_p), ws.ptr, ws.nbytes,
+                                            _stream_ptr(stream)), "hk_hankel_shard_forward_p2p")
+
+
+def shard_finish_p2p(ws: ShardWorkspace, g, recv, y_mag_ptrs, y_sign_ptrs, stream=None):
+    """Phase 2 of rank g with the y all-gather fused into K3's stores: y_*_ptrs[d] = rank d's padded
+    y buffers (y_rows rows)."""
+    import torch
+    if len(y_mag_ptrs) != ws.G or len(y_sign_ptrs) != ws.G:
+        raise ValueError("need one y pointer per rank")
+    r = _dev_ptr(recv, (torch.int32,), (ws.info["buffer_words"],), "recv")
+    am, asg = _ptr_array(y_mag_ptrs), _ptr_array(y_sign_ptrs)
+    _check(_lib.hk_hankel_shard_finish_p2p(ws.kind, ws.n, ws.P, ws.G, int(g), r,
+                                           ctypes.cast(am, ctypes.c_void_p),
+                                           ctypes.cast(asg, ctypes.c_void_p), ws.ptr, ws.nbytes,
+                                           _stream_ptr(stream)), "hk_hankel_shard_finish_p2p")
 
 
 class HostPipeline:

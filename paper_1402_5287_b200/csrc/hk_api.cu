@@ -632,6 +632,50 @@ int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, in
     return launch_k3_range(prm, stream, row0, nrows);
 }
 
+int32_t hk_hankel_shard_forward_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                    const uint64_t *a_mag, const int8_t *a_sign,
+                                    const uint64_t *x_mag, const int8_t *x_sign,
+                                    uint32_t *const *recv_ptrs, void *ws, size_t ws_bytes,
+                                    void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !recv_ptrs) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    for (int d = 0; d < G; ++d) {
+        if (!recv_ptrs[d]) return HK_EINVAL;
+        prm.peer_recv[d] = recv_ptrs[d];
+    }
+    prm.p2p = 1;
+    prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
+    prm.Yhat = recv_ptrs[g];  // unused by the p2p stores; a valid buffer of this rank
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    return launch_ntt_path(prm, stream, HK_STAGE_SLICE_ROWS | HK_STAGE_COLUMNS);
+}
+
+int32_t hk_hankel_shard_finish_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                   const uint32_t *recv, uint64_t *const *y_mag_ptrs,
+                                   int8_t *const *y_sign_ptrs, void *ws, size_t ws_bytes,
+                                   void *stream) {
+    if (!recv || !y_mag_ptrs || !y_sign_ptrs) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    for (int d = 0; d < G; ++d) {
+        if (!y_mag_ptrs[d] || !y_sign_ptrs[d]) return HK_EINVAL;
+        prm.peer_ymag[d] = y_mag_ptrs[d];
+        prm.peer_ysign[d] = y_sign_ptrs[d];
+    }
+    prm.p2p = 1;
+    prm.Yhat = const_cast<uint32_t *>(recv);
+    prm.y_mag = y_mag_ptrs[g]; prm.y_sign = y_sign_ptrs[g];
+    const int64_t row0 = prm.shard_row0;
+    const int64_t nrows = (n - row0) < pl.rpr ? (n - row0) : pl.rpr;
+    return launch_k3_range(prm, stream, row0, nrows);
+}
+
 int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                      const int8_t *a_sign, void *ws, size_t ws_bytes, void *stream) {
     if (!a_mag || !a_sign || !ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;

@@ -12,7 +12,8 @@ constexpr int kNumPrimes = 5;
 constexpr uint64_t kWsMagic = 0x484b5753504c414eull;  // "HKWSPLAN"
 constexpr int kMaxLogN1 = 15;                           // N1 <= 32768 (K2 register budget)
 constexpr int kMinLogN1 = 6;
-constexpr int kSplitLogN1 = 15;                         // K2 as prepare + prepared launches from here
+constexpr int kSplitLogN1 = 15;
+constexpr int kMaxShards = 8;                           // sigma-coset shards G <= 8                         // K2 as prepare + prepared launches from here
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
@@ -62,6 +63,13 @@ struct Params {
     int64_t shard_row0;          // K3: first internal row of this rank's block (g * rpr)
     int64_t y_rows;              // rows of the y buffer (m, or G * rpr when sharded)
     int32_t round_out;           // F4: y = round_half_even(Y / 2^P) in L + 1 limbs (2^-P scale)
+    // peer-memory exchange (P2P shards): K2 stores row block r of its columns straight into rank
+    // r's receive buffer, K3 stores its y rows into every rank's y buffer (pointers mapped into
+    // this process, e.g. torch symmetric memory over NVLink); 0 = buffers of this rank only
+    int32_t p2p;
+    uint32_t *peer_recv[kMaxShards];
+    uint64_t *peer_ymag[kMaxShards];
+    int8_t *peer_ysign[kMaxShards];
     // inputs / outputs (device)
     const uint64_t *a_mag;
     const int8_t *a_sign;

@@ -144,12 +144,17 @@ HK_DEV void dit_bottom_regs(uint32_t (&v)[1 << RL], const uint2 *tw, uint32_t p)
 // shards, the all-to-all send buffer [dest rank][column][rpr]: row block i / rpr goes to rank
 // i / rpr (to rank G - 1 - i / rpr when the rows are reversed, Toeplitz, so that every rank's
 // final y rows form block `rank` of the padded y and the all-gather is in rank order).
+// With peer-memory exchange (prm.p2p) the chunk goes straight into rank dst's receive buffer, at
+// this rank's (source) chunk slot -- the all-to-all fused into K2's stores.
 template <bool SHARD>
 HK_DEV uint32_t *yhat_at(const Params &prm, size_t cidx, int i) {
     if constexpr (!SHARD) return prm.Yhat + cidx * prm.ldY + i;
     const unsigned rpr = (unsigned)prm.shard_rpr, blk = (unsigned)i / rpr;
     const unsigned dst = prm.reverse_out ? (1u << prm.shard_gamma) - 1u - blk : blk;
-    return prm.Yhat + ((size_t)dst * kNumPrimes * prm.n2loc + cidx) * rpr + ((unsigned)i - blk * rpr);
+    const size_t chunk = (size_t)kNumPrimes * prm.n2loc;
+    if (prm.p2p)
+        return prm.peer_recv[dst] + ((size_t)prm.k1_block * chunk + cidx) * rpr + ((unsigned)i - blk * rpr);
+    return prm.Yhat + ((size_t)dst * chunk + cidx) * rpr + ((unsigned)i - blk * rpr);
 }
 
 // Top inverse pass (R = 5, S = N/32) with the result going to HBM (or back to smem for fold).
@@ -267,6 +272,7 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         }
         __syncthreads();
     }
+    if (SHARD && prm.p2p) __threadfence_system();  // peer stores visible before the next barrier
 }
 
 // Inverse passes above the bottom one, output to Y^ (shared by the full and prepared bodies).
@@ -288,6 +294,7 @@ HK_DEV void k2_inverse_tail(const Params &prm, uint32_t *sm, const uint2 *twf, u
         }
         __syncthreads();
     }
+    if (SHARD && prm.p2p) __threadfence_system();  // peer stores visible before the next barrier
 }
 
 // F1 prepare: A^'s forward column transform only, stored to AT in the bottom-pass register

@@ -645,14 +645,19 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
         if (orow_r >= m) break;
         const int64_t orow = prm.reverse_out ? (prm.y_rows - 1 - orow_r) : orow_r;
         if (!prm.round_out) {
-            uint64_t *yo = prm.y_mag + orow * Ly;
-            for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
-            if (tid == 0)
-                prm.y_sign[orow] = s_neg[rr] ? (int8_t)-1 : (s_zmin[rr] < Ly ? (int8_t)1 : (int8_t)0);
+            const int8_t sgn = s_neg[rr] ? (int8_t)-1 : (s_zmin[rr] < Ly ? (int8_t)1 : (int8_t)0);
+            // peer-memory exchange: the y all-gather fused into the stores (every rank's y buffer)
+            const int ndst = prm.p2p ? (1 << prm.shard_gamma) : 1;
+            for (int d = 0; d < ndst; ++d) {
+                uint64_t *yo = (prm.p2p ? prm.peer_ymag[d] : prm.y_mag) + orow * Ly;
+                for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
+                if (tid == 0) (prm.p2p ? prm.peer_ysign[d] : prm.y_sign)[orow] = sgn;
+            }
         } else {
             k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0, orow);
         }
     }
+    if (prm.p2p) __threadfence_system();  // peer y stores visible before the next barrier
     (void)row;
 }
 

@@ -5,7 +5,11 @@
   its N2/G columns per prime and writes per-destination row-block chunks; one all-to-all moves
   Y^ from column ownership to row ownership; rank g finishes its row block (K3); an all-gather of
   the equal-size y blocks gives every rank y.  Compute per rank ~1/G of K2/K3 and of K1's
-  transforms (slicing is replicated).
+  transforms (slicing is replicated).  With peer memory (torch symmetric memory over NVLink,
+  the default when available) both exchanges are fused into the kernels' stores: K2 writes each
+  row-block chunk straight into the destination rank's receive buffer and K3 writes its y rows
+  into every rank's y; a device-side barrier follows each phase.  Otherwise NCCL
+  all_to_all_single / all_gather_into_tensor do the exchanges.
 * ShardedHankel -- plan P-3, north_star's literal row-block sharding (below).
 
 One process per GPU (torchrun), torch.distributed for the plumbing (NCCL over NVLink on GPUs,
@@ -19,6 +23,8 @@ The per-shard compute is a parameter so the sharding / gather logic can be exerc
 (gloo) with any exact shard function; the default is the CUDA path.
 """
 from __future__ import annotations
+
+import os
 
 import numpy as np
 
@@ -134,7 +140,7 @@ class CosetShardedMatvec:
     on CPU (gloo), with ``info`` the layout (paper_1402_5287_b200.shard_plan)."""
 
     def __init__(self, kind, a_mag, a_sign, x_mag, x_sign, P, group=None, forward=None,
-                 finish=None, info=None):
+                 finish=None, info=None, p2p="auto"):
         import torch
         import torch.distributed as dist
         self.dist, self.group = dist, group
@@ -155,21 +161,84 @@ class CosetShardedMatvec:
         words, rpr, yr = info["buffer_words"], info["rows_per_rank"], info["y_rows"]
         self.rpr, self.y_rows = int(rpr), int(yr)
         Ly = 2 * ((P + 63) // 64) + 1
-        self.send = torch.zeros((words,), dtype=torch.int32, device=dev)
-        self.recv = torch.zeros((words,), dtype=torch.int32, device=dev)
-        self.y_pad = torch.zeros((yr, Ly), dtype=a_mag.dtype, device=dev)
-        self.s_pad = torch.zeros((yr,), dtype=torch.int8, device=dev)
+        self.p2p = False
+        if os.environ.get("HK_P2P", "1") == "0":
+            p2p = False
+        if p2p and self.ws is not None and self.G > 1:
+            # every rank takes the same decision: setup steps are agreed on with MIN all-reduces,
+            # so a rank that cannot map peer memory never leaves the others in a rendezvous
+            self.p2p = self._setup_p2p(words, yr, Ly, a_mag.dtype, dev)
+            if not self.p2p and p2p != "auto":
+                raise RuntimeError("peer-memory exchange requested but unavailable")
+        if not self.p2p:
+            self.send = torch.zeros((words,), dtype=torch.int32, device=dev)
+            self.recv = torch.zeros((words,), dtype=torch.int32, device=dev)
+            self.y_pad = torch.zeros((yr, Ly), dtype=a_mag.dtype, device=dev)
+            self.s_pad = torch.zeros((yr,), dtype=torch.int8, device=dev)
+
+    def _agree(self, ok: bool, dev) -> bool:
+        import torch
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item())
+
+    def _setup_p2p(self, words, yr, Ly, mag_dtype, dev) -> bool:
+        """Receive buffer and padded y in torch symmetric memory (NVLink peer-mapped): the
+        all-to-all is fused into K2's stores and the y all-gather into K3's stores."""
+        import torch
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            recv = symm_mem.empty(words, dtype=torch.int32, device=dev)
+            y_pad = symm_mem.empty(yr, Ly, dtype=mag_dtype, device=dev)
+            s_pad = symm_mem.empty(yr, dtype=torch.int8, device=dev)
+            ok = True
+        except Exception:
+            ok = False
+        if not self._agree(ok, dev):
+            return False
+        try:
+            grp = self.group if self.group is not None else self.dist.group.WORLD
+            handles = [symm_mem.rendezvous(t, grp) for t in (recv, y_pad, s_pad)]
+
+            def peer_ptrs(t, h):
+                off = t.data_ptr() - int(h.buffer_ptrs[self.rank])
+                return [int(p) + off for p in h.buffer_ptrs]
+
+            ptrs = [peer_ptrs(t, h) for t, h in zip((recv, y_pad, s_pad), handles)]
+            ok = all(len(p) == self.G and all(p) for p in ptrs)
+        except Exception:
+            ok = False
+        if not self._agree(ok, dev):
+            return False
+        self.recv, self.y_pad, self.s_pad = recv, y_pad, s_pad
+        self.recv_ptrs, self.y_ptrs, self.s_ptrs = ptrs
+        self.h_recv, self.h_y = handles[0], handles[1]
+        return True
 
     def compute_forward(self):
-        self.forward(self.ws, self.rank, *self.inputs, self.send)
+        if self.p2p:
+            from . import shard_forward_p2p
+            shard_forward_p2p(self.ws, self.rank, *self.inputs, self.recv_ptrs)
+        else:
+            self.forward(self.ws, self.rank, *self.inputs, self.send)
 
     def exchange(self):
-        self.dist.all_to_all_single(self.recv, self.send, group=self.group)
+        if self.p2p:  # every rank's K2 stores into this rank's receive buffer are done
+            self.h_recv.barrier()
+        else:
+            self.dist.all_to_all_single(self.recv, self.send, group=self.group)
 
     def compute_finish(self):
-        self.finish(self.ws, self.rank, self.recv, self.y_pad, self.s_pad)
+        if self.p2p:
+            from . import shard_finish_p2p
+            shard_finish_p2p(self.ws, self.rank, self.recv, self.y_ptrs, self.s_ptrs)
+        else:
+            self.finish(self.ws, self.rank, self.recv, self.y_pad, self.s_pad)
 
     def gather(self):
+        if self.p2p:  # every rank's K3 stores into this rank's y are done
+            self.h_y.barrier()
+            return
         r0, r1 = self.rank * self.rpr, (self.rank + 1) * self.rpr
         d = self.dist
         try:  # in place: this rank's block already sits in its slot of the output

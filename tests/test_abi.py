@@ -19,7 +19,7 @@ PRIMES = [2147352577, 2146959361, 2146041857, 2144468993, 2142502913]
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "hk.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(hk_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(hk_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():

@@ -93,3 +93,41 @@ def test_shard_plan_rejects_bad_G(hk):
             hk.shard_plan(0, 100, 4200, G)
     with pytest.raises(hk.HKError):  # N2 / G < 32 (P = 1000 -> N2 = 32)
         hk.shard_plan(0, 100, 1000, 2)
+
+
+def sharded_p2p(hk, kind, G, am, asg, xm, xsg, P):
+    """The peer-memory variant with G emulated ranks on one GPU: every rank's K2 writes straight
+    into the other ranks' receive buffers and every rank's K3 into all ranks' y buffers (the
+    pointers a multi-GPU run maps over NVLink are plain local pointers here)."""
+    n = xm.shape[0]
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    wss = [hk.ShardWorkspace(kind, n, P, G) for _ in range(G)]
+    info = wss[0].info
+    yr, Ly = info["y_rows"], hk.out_limbs(P)
+    recv = [torch.full((info["buffer_words"],), -1, dtype=torch.int32, device="cuda") for _ in range(G)]
+    ym = [torch.full((yr, Ly), -7, dtype=torch.int64, device="cuda") for _ in range(G)]
+    ys = [torch.full((yr,), 9, dtype=torch.int8, device="cuda") for _ in range(G)]
+    rp = [t.data_ptr() for t in recv]
+    for g in range(G):
+        hk.shard_forward_p2p(wss[g], g, a, sa, x, sx, rp)
+    torch.cuda.synchronize()  # the barrier between the phases
+    for g in range(G):
+        hk.shard_finish_p2p(wss[g], g, recv[g], [t.data_ptr() for t in ym], [t.data_ptr() for t in ys])
+    torch.cuda.synchronize()
+    for g in range(G):
+        assert wss[g].status() == hk.HK_OK
+    outs = []
+    for d in range(G):  # every rank holds the whole y
+        m_, s_ = (ym[d][yr - n:], ys[d][yr - n:]) if kind == gen.TOEPLITZ else (ym[d][:n], ys[d][:n])
+        outs.append(hk.to_host(m_, s_))
+    return outs
+
+
+@pytest.mark.parametrize("kind,n,P,G", [(0, 100, 4200, 2), (1, 130, 8000, 8), (2, 77, 9000, 4),
+                                        (0, 5, 17000, 8), (2, 128, 2100, 2)])
+def test_coset_shards_p2p_match_oracle(hk, kind, n, P, G):
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=90 + n + G)
+    want = oracle.matvec(kind, P, am, asg, xm, xsg)
+    for got in sharded_p2p(hk, kind, G, am, asg, xm, xsg, P):
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])

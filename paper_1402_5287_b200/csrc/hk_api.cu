@@ -91,7 +91,7 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     in.Ly = 2 * in.L + 1;
     in.k_primes = kNumPrimes;
     in.a_count = kind == HK_CIRCULANT ? n : m + n - 1;
-    if (in.Ly > kK3Threads * kK3MaxChunk) return HK_EUNSUPPORTED;
+    if (in.Ly > kK3MaxLy) return HK_EUNSUPPORTED;
     // matrix-index transform length
     int64_t need;
     if (kind == HK_CIRCULANT) {
@@ -123,7 +123,7 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     bool found = false;
     // Smallest N2 first; for it the widest slice w in {65, 64} that satisfies the capacity bound.
     // w >= 64 makes the limb index floor(w s / 64) of coefficient s injective, which the carry
-    // kernel (K3b) relies on.
+    // kernel (K3) relies on.
     for (int lg2 = kMinLogN2; lg2 <= kMaxLogN2 && !found; ++lg2) {
         for (int64_t w = kMaxW; w >= 64 && !found; --w) {
             const int64_t Ls = (P + w - 1) / w;

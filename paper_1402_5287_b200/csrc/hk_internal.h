@@ -17,8 +17,8 @@ constexpr int kMaxShards = 8;                           // sigma-coset shards G 
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
-constexpr int kK3Threads = 320;                         // K3 block (carry: one output row at a time)
-constexpr int kK3MaxChunk = 7;                          // limbs per thread -> Ly <= 2240
+constexpr int kK3MaxLy = 2240;                          // K3 carry: 320 threads, <= 14 limbs per
+                                                        // thread over 4 rows / 2 rows (N2 = 2048)
 
 struct PrimeConsts {
     uint32_t p, pneg;          // modulus, -p^-1 mod 2^32 (Montgomery)

@@ -85,9 +85,15 @@ def alg_counts(plan, m=None):
     pointwise = k * N2 * N1
     k2_instr = I_GS * bf_col_fwd + I_CT * bf_col_inv + I_MONT * pointwise
     k2_bfly_eq = (C_GS * bf_col_fwd + C_CT * bf_col_inv + C_MONT * pointwise) / C_GS
+    # K1: slice NTTs of a and x (GS) + 2 Shoup products per slice residue; K3: inverse slice NTTs
+    # (CT) + Garner CRT per output coefficient (10 Shoup products = 80 FMA clocks + ~10 IMAD.WIDE
+    # = 40 -> 120 clocks = 15 GS-eq); carries are ALU work and not counted
+    residues = k * (rows_a + n) * plan["Ls"]
+    k1_bfly_eq = bf_row_fwd + 2 * residues
+    k3_bfly_eq = (C_CT * bf_row_inv) / C_GS + 15 * m * (2 * plan["Ls"] - 1)
     return dict(bf_row_fwd=bf_row_fwd, bf_col_fwd=bf_col_fwd, bf_col_inv=bf_col_inv,
                 bf_row_inv=bf_row_inv, pointwise=pointwise, k2_instr=k2_instr,
-                k2_bfly_eq=k2_bfly_eq,
+                k2_bfly_eq=k2_bfly_eq, k1_bfly_eq=k1_bfly_eq, k3_bfly_eq=k3_bfly_eq,
                 butterflies=bf_row_fwd + bf_col_fwd + bf_col_inv + bf_row_inv)
 
 
@@ -460,6 +466,15 @@ def main():
                             "frac": (ach_instr / peak_tinstr) if ach_instr else None,
                             "per_unit": f"{I_GS}/GS, {I_CT}/CT, {I_MONT}/Montgomery SASS instructions"},
             "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms_step}
+    if world == 1:  # the same integer-pipe model for the other two kernels (CUDA-event times)
+        roof["other_kernels"] = {
+            name: {"algorithmic_per_launch": cnt[key], "kernel_ms": ms_,
+                   "achieved": cnt[key] / (ms_ * 1e-3) / 1e12,
+                   "frac": cnt[key] / (ms_ * 1e-3) / 1e12 / peak_bfly}
+            for name, key, ms_ in (("k1_slice_rowntt", "k1_bfly_eq", stage_ms[0]),
+                                   ("k3_finish", "k3_bfly_eq", stage_ms[2]))}
+        roof["other_kernels"]["per_unit"] = ("K1: GS butterflies + 2 per slice residue; K3: CT 9/8 + "
+                                             "15 per Garner CRT (GS-butterfly equivalents)")
     hbm_peak = float(peaks.get("hbm_gbs", 6549.4))
     roof["hbm_check"] = {"alg_bytes_per_step": all_bytes,
                          "achieved_gbs": all_bytes / (ms_step * 1e-3) / 1e9, "peak_gbs": hbm_peak}

@@ -299,8 +299,17 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params
 // (prime, sigma) column segment; the pad keeps the contiguous (S = 1, radix 32: lanes 32 sigma
 // apart) and the strided (S >= 32 / R) passes and the Garner pairs bank-conflict-free, and it is
 // separable (pad(B + j0 + m S) = pad(B + j0) + pad(m S)) so per-point offsets are immediates.
+#ifndef HK_K3_ROWS
+#define HK_K3_ROWS 4   // output rows per K3 tile (N2 <= 1024)
+#endif
+#ifndef HK_K3_BLOCK
+#define HK_K3_BLOCK 320
+#endif
+#ifndef HK_K3_MINB
+#define HK_K3_MINB 2
+#endif
 template <int LOGN2>
-constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : 4; }
+constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : HK_K3_ROWS; }
 
 template <int LOGN2>
 struct K3Layout {
@@ -361,7 +370,7 @@ HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint32_t (&c
     cw[0] = a0; cw[1] = a1; cw[2] = a2; cw[3] = a3; cw[4] = a4;
 }
 
-constexpr int kK3Block = 320;  // 5 primes x 4 rows x 32 groups = 2 radix-32 groups per thread
+constexpr int kK3Block = HK_K3_BLOCK;  // 320: 5 primes x 4 rows x 32 groups = 2 radix-32 groups per thread
 
 // Inverse DIT pass of radix 2^RR at stride S over all (prime, row) transforms of the tile.
 template <int LOGN2, int RR, int S>
@@ -463,7 +472,7 @@ HK_DEV void k3_store_rounded(const Params &prm, const uint64_t *M, bool neg, int
 }
 
 template <int LOGN2, int CH>  // CH = limbs per thread = ceil(Ly / (kK3Block / R))
-__global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
+__global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     using LY = K3Layout<LOGN2>;
     constexpr int N2 = 1 << LOGN2, R = LY::R, T = kK3Block;
     extern __shared__ uint32_t sm[];  // residues -> CRT words [5][N2][R] (swizzled) -> y rows [R][Ly]
@@ -487,7 +496,8 @@ __global__ void __launch_bounds__(kK3Block, 2) k3_finish(Params prm) {
             }
             uint32_t *d = sm + LY::idx(kp, sg, 0);
             if (vec) {
-                if constexpr (R == 4) cp_async16(d, g);
+                if constexpr (R == 8) { cp_async16(d, g); cp_async16(d + 4, g + 4); }
+                else if constexpr (R == 4) cp_async16(d, g);
                 else cp_async8(d, g);
             } else {
 #pragma unroll

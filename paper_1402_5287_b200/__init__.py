@@ -20,8 +20,14 @@ import numpy as np
 
 from ._build import LIB as _LIB_PATH
 
-# dev A/B only: load an alternative in-tree build of the same library (scripts/gpu_ab.sh)
-_LIB_PATH = os.environ.get("HK_LIB_VARIANT", _LIB_PATH)
+# dev A/B only (scripts/gpu_ab.sh): an alternative build of the same library, accepted only from
+# this package's lib/ directory
+_variant = os.environ.get("HK_LIB_VARIANT")
+if _variant:
+    _libdir = os.path.realpath(os.path.dirname(_LIB_PATH))
+    if not os.path.realpath(_variant).startswith(_libdir + os.sep):
+        raise ImportError(f"HK_LIB_VARIANT must name a build under {_libdir}")
+    _LIB_PATH = _variant
 
 HK_OK, HK_EINVAL, HK_ERANGE, HK_ENOMEM, HK_EUNSUPPORTED, HK_ECUDA = 0, -1, -2, -3, -4, -5
 HANKEL, TOEPLITZ, CIRCULANT = 0, 1, 2

@@ -402,3 +402,17 @@ def test_split_k2_large_n1(hk):
     hk.matvec(0, *hk.to_device(am, asg), *hk.to_device(xm, xsg), P, ws=A.ws)  # cold call, same ws
     with pytest.raises(hk.HKError):
         A.matvec(*hk.to_device(x2m, x2s))
+
+
+@pytest.mark.parametrize("kind,n,P", [(0, 33, 33281), (1, 20, 40000), (2, 64, 66560), (0, 7, 66000)])
+def test_large_P_slice_transform_2048(hk, kind, n, P):
+    """P > 33,280 bits: slice transform N2 = 2048 (K1 / K3 instances with LOGN2 = 11, K3 tiles of
+    2 rows), up to the planner's limit P = 66,560 (Ls = 1024)."""
+    assert hk.plan(kind, n, P)["log_n2"] == 11
+    full_case(hk, kind, n, P, seed=P % 97)
+    full_case(hk, kind, n, P, seed=P % 89, recipe="carry_stress")
+
+
+def test_planner_limit(hk):
+    with pytest.raises(hk.HKError):
+        hk.plan(0, 10, 66561)

@@ -16,14 +16,17 @@
 
 namespace hk {
 
+// N1 = 2^14 (C3): 256 threads (two top-pass groups each), 2 CTAs per SM, no A^ staging: two
+// independent columns per SM desynchronise their barrier / load / arithmetic phases, which beats
+// one 512-thread CTA with A^ staged in smem (0.70 vs 0.76 ms at C3) despite 148 B of spills
 #ifndef HK_K2_T14
-#define HK_K2_T14 512  // threads per CTA at N1 = 2^14
+#define HK_K2_T14 256  // threads per CTA at N1 = 2^14
 #endif
 #ifndef HK_K2_MINB14
-#define HK_K2_MINB14 1  // resident CTAs per SM at N1 = 2^14
+#define HK_K2_MINB14 2  // resident CTAs per SM at N1 = 2^14
 #endif
 #ifndef HK_K2_STAGE14
-#define HK_K2_STAGE14 1  // stage the A^ column in smem by cp.async at N1 = 2^14
+#define HK_K2_STAGE14 0  // stage the A^ column in smem by cp.async at N1 = 2^14
 #endif
 template <int LOGN1>
 constexpr int k2_threads() {

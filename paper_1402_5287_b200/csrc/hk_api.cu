@@ -466,7 +466,7 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
          cudaStreamWaitEvent(s1, e0, 0) == cudaSuccess && cudaStreamWaitEvent(s2, e0, 0) == cudaSuccess;
     ok = ok && cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), s0) == cudaSuccess;
     const int ga = k1_tiles_a(prm), gx = k1_tiles_x(prm);
-    const int kTile = 8;  // rows per K1 tile (kK1Rows)
+    const int kTile = k1_tile_rows();
     struct Chunk { int t0, nt; };
     Chunk chunks[6];
     int nch = 0;

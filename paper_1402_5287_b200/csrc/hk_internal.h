@@ -107,6 +107,7 @@ int launch_init(const Params &prm, const uint32_t *gens, void *stream);
 int launch_ntt_path(const Params &prm, void *stream, uint32_t stages);
 // partial launches for the pipelined host path: K1 over tiles [tile0, tile0 + ntiles) of the
 // combined [a | x] tile index (8 rows per tile), K3 over output rows [row0, row0 + nrows)
+int k1_tile_rows();  // entries per K1 tile
 int k1_tiles_a(const Params &prm);
 int k1_tiles_x(const Params &prm);
 int launch_k1_range(const Params &prm, void *stream, int tile0, int ntiles);

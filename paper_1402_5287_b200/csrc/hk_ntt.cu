@@ -76,7 +76,13 @@ constexpr int k1_row_stride() {  // = 4 (mod 32): transposed [row][sigma] tiles 
 // w-bit digits of its top-pass group once (registers), then for every prime: residues -> top
 // DIF pass (radix 2^5, upper half zero) in registers -> smem -> remaining passes -> transposed
 // write of [prime][sigma][row] (kK1Rows consecutive rows per sigma = one 32-byte sector).
-constexpr int kK1Rows = 8;
+#ifndef HK_K1_ROWS
+#define HK_K1_ROWS 8
+#endif
+#ifndef HK_K1_MINB
+#define HK_K1_MINB 3
+#endif
+constexpr int kK1Rows = HK_K1_ROWS;
 template <int LOGN2>
 constexpr int k1_threads() {
     return kK1Rows * ((1 << LOGN2) / 32 > 8 ? (1 << LOGN2) / 32 : 8);
@@ -89,7 +95,7 @@ constexpr int k1_threads() {
 // Block b holds the transform outputs at bit-reversed positions [b N2 / G, (b + 1) N2 / G), the
 // frequencies congruent to bitrev(b) mod G.
 template <int LOGN2, int GAMMA>
-__global__ void __launch_bounds__(k1_threads<LOGN2>(), 3) k1_slice_rowntt(Params prm, int tiles_a) {
+__global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rowntt(Params prm, int tiles_a) {
     constexpr int N2 = 1 << LOGN2;
     constexpr int BL = N2 >> GAMMA;          // outputs kept per row and prime
     constexpr int GK = 32 >> GAMMA;          // top-pass points kept per group
@@ -796,6 +802,7 @@ int launch_k2_mode(const Params &prm, void *stream, int mode) {
     }
 }
 
+int k1_tile_rows() { return kK1Rows; }
 int k1_tiles_a(const Params &prm) { return (int)((prm.a_count + kK1Rows - 1) / kK1Rows); }
 int k1_tiles_x(const Params &prm) { return (int)((prm.n + kK1Rows - 1) / kK1Rows); }
 

@@ -45,6 +45,8 @@ I_GS, I_CT, I_MONT = 7, 8, 4
 # 10 (2 IMAD.WIDE + IMAD).  Peak = 4 SMSPs x 32 lanes / 8 clocks = 16 GS butterflies/clk/SM.
 C_GS, C_CT, C_MONT = 8, 9, 10
 BFLY_PER_CLK_SM = 16
+# measured register-resident ceilings (scripts/micro_bfly.cu, profiles/r01/micro_bfly.log)
+MICRO_GS, MICRO_CT = 12.07, 11.22  # butterflies / clk / SM
 
 
 def parse():
@@ -462,6 +464,12 @@ def main():
             "algorithmic_per_launch": cnt["k2_bfly_eq"],
             "per_unit": f"GS butterfly 1, CT butterfly {C_CT}/{C_GS}, Montgomery product {C_MONT}/{C_GS} "
                         "(minimal integer-pipe clocks relative to GS); full transforms, no pruning credit",
+            "vs_microbenchmark": (
+                None if k2_ms <= 0 else
+                (cnt["bf_col_fwd"] / MICRO_GS + cnt["bf_col_inv"] / MICRO_CT +
+                 cnt["pointwise"] * C_MONT / C_GS / MICRO_GS) / (nsm * sm_max * 1e6) / (k2_ms * 1e-3)),
+            "vs_microbenchmark_note": ("K2 time vs its butterflies at the register-resident loop rates of "
+                                       "scripts/micro_bfly.cu (GS 12.07, CT 11.22 per clk per SM)"),
             "issue_model": {"achieved": ach_instr, "peak": peak_tinstr, "unit": "Tinstr/s",
                             "frac": (ach_instr / peak_tinstr) if ach_instr else None,
                             "per_unit": f"{I_GS}/GS, {I_CT}/CT, {I_MONT}/Montgomery SASS instructions"},

@@ -430,6 +430,49 @@ def main():
                "single_call_api": "hk_matvec_host (synchronous)"}
         del pipe
 
+    # ---- e2e at N > 1: every step each rank copies its (replicated) a and x from pinned host memory,
+    # the sharded step runs, rank 0 reads y back; host wall clock between barriers, max over ranks
+    if world > 1 and not args.no_e2e:
+        pa = torch.from_numpy(am.view(np.int64)).pin_memory()
+        ps = torch.from_numpy(asg).pin_memory()
+        px = torch.from_numpy(xm.view(np.int64)).pin_memory()
+        pxs = torch.from_numpy(xsg).pin_memory()
+        ym_h, ys_h = None, None
+        Ke = max(3, min(K, 20))
+
+        def e2e_step():
+            a.copy_(pa, non_blocking=True)
+            sa.copy_(ps, non_blocking=True)
+            x.copy_(px, non_blocking=True)
+            sx.copy_(pxs, non_blocking=True)
+            step()
+            if rank == 0:
+                y_dev, s_dev = sh.result()
+                nonlocal ym_h, ys_h
+                if ym_h is None:
+                    ym_h = torch.empty(y_dev.shape, dtype=y_dev.dtype).pin_memory()
+                    ys_h = torch.empty(s_dev.shape, dtype=s_dev.dtype).pin_memory()
+                ym_h.copy_(y_dev, non_blocking=True)
+                ys_h.copy_(s_dev, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(2):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(Ke):
+            e2e_step()
+        dist.barrier()
+        tt = torch.tensor([(time.perf_counter() - t0) * 1e3 / Ke], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_e2e = float(tt.item())
+        Ly = plan["Ly"]
+        e2e = {"value": 1000.0 / ms_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(world * (am.nbytes + asg.nbytes + xm.nbytes + xsg.nbytes)),
+               "d2h_bytes_per_step": int(n * Ly * 8 + n), "ms_per_step": ms_e2e, "steps": Ke,
+               "api": "every rank: H2D of a, x into its device inputs; the sharded step; rank 0: D2H of y",
+               "timing": "host wall clock between barriers, max over ranks (synchronous steps)"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

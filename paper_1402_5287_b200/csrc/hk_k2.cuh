@@ -25,6 +25,12 @@ namespace hk {
 #ifndef HK_K2_MINB14
 #define HK_K2_MINB14 2  // resident CTAs per SM at N1 = 2^14
 #endif
+#ifndef HK_K2_L2PF
+#define HK_K2_L2PF 1  // bulk-prefetch the A^ column into L2 when it is not staged in smem
+#endif
+#ifndef HK_K2_L2PF_NEXT
+#define HK_K2_L2PF_NEXT 148  // columns ahead whose X^ is also prefetched into L2 (0: off)
+#endif
 #ifndef HK_K2_STAGE14
 #define HK_K2_STAGE14 0  // stage the A^ column in smem by cp.async at N1 = 2^14
 #endif
@@ -219,6 +225,17 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         const int nch = (int)prm.ldA >> 2;  // the zero-padded column (ldA = N1 or N1 / 2)
         const uint32_t *g = prm.Ahat + cidx * prm.ldA;
         for (int c = tid; c < nch; c += T) cp_async16(sA + 4 * c, g + 4 * c);
+    } else if (HK_K2_L2PF && tid == 0) {
+        // no staging room: have the A^ column brought into L2 (bulk prefetch) during X^'s transform
+        const uint32_t *g = prm.Ahat + cidx * prm.ldA;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g),
+                     "r"((unsigned)(prm.ldA * 4)) : "memory");
+        if (HK_K2_L2PF_NEXT) {  // and the X^ column of a CTA about one wave ahead
+            const size_t nxt = cidx + HK_K2_L2PF_NEXT;
+            if (nxt < (size_t)kNumPrimes * prm.n2loc)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(prm.Xhat + nxt * prm.ldX),
+                             "r"((unsigned)(prm.ldX * 4)) : "memory");
+        }
     }
 
     // ---- X^: forward, bottom pass kept in registers

@@ -83,6 +83,9 @@ constexpr int k1_row_stride() {  // = 4 (mod 32): transposed [row][sigma] tiles 
 #define HK_K1_MINB 3
 #endif
 constexpr int kK1Rows = HK_K1_ROWS;
+#ifndef HK_K1_L2PF
+#define HK_K1_L2PF 148  // tiles ahead whose limbs are bulk-prefetched into L2 (0: off)
+#endif
 template <int LOGN2>
 constexpr int k1_threads() {
     return kK1Rows * ((1 << LOGN2) / 32 > 8 ? (1 << LOGN2) / 32 : 8);
@@ -139,6 +142,18 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         char *d = reinterpret_cast<char *>(slimb);
         for (int64_t c = tid; c < bytes / 16; c += T) cp_async16(d + 16 * c, g + 16 * c);
         if ((bytes & 15) && tid == 0) cp_async8(d + (bytes & ~int64_t(15)), g + (bytes & ~int64_t(15)));
+        if (HK_K1_L2PF && tid == 0) {  // bring the limbs of the tile one wave ahead into L2
+            const int bt2 = bt + HK_K1_L2PF;
+            const bool x2 = bt2 >= tiles_a;
+            const int64_t cnt2 = x2 ? prm.n : prm.a_count;
+            const int64_t q0 = (int64_t)(x2 ? bt2 - tiles_a : bt2) * kK1Rows;
+            if (q0 < cnt2) {
+                const int64_t nr2 = cnt2 - q0 < kK1Rows ? cnt2 - q0 : kK1Rows;
+                const uint64_t *g2 = (x2 ? prm.x_mag : prm.a_mag) + q0 * L;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g2),
+                             "r"((unsigned)(nr2 * L * 8) & ~15u) : "memory");
+            }
+        }
         cp_async_wait_all();
         __syncthreads();
     }

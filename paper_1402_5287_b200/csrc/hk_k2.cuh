@@ -351,6 +351,14 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
     const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     const int nx = (int)prm.n;
+    if (HK_K2_L2PF && tid == 0) {  // the stored A^ transform of this column and the next wave's X^
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(prm.AT + cidx * N1),
+                     "r"((unsigned)(N1 * 4)) : "memory");
+        const size_t nxt = cidx + HK_K2_L2PF_NEXT;
+        if (HK_K2_L2PF_NEXT && nxt < (size_t)kNumPrimes * prm.n2loc)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(prm.Xhat + nxt * prm.ldX),
+                         "r"((unsigned)(prm.ldX * 4)) : "memory");
+    }
     k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
     K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     const uint32_t *at = prm.AT + cidx * N1;

@@ -131,3 +131,19 @@ def test_coset_shards_p2p_match_oracle(hk, kind, n, P, G):
     want = oracle.matvec(kind, P, am, asg, xm, xsg)
     for got in sharded_p2p(hk, kind, G, am, asg, xm, xsg, P):
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("G,p2p", [(2, False), (8, True)])
+def test_coset_shards_split_k2(hk, G, p2p):
+    """N1 = 2^15 (n > 8192): the shard K2 runs as prepare + prepared-shard launches (MODE 1 + 4).
+    Checked against the single-GPU call (itself bit-exact vs the oracle) and by fingerprints."""
+    kind, n, P = 0, 8200, 4200
+    assert hk.plan(kind, n, P)["log_n1"] == 15
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=8)
+    got = (sharded_p2p(hk, kind, G, am, asg, xm, xsg, P)[G - 1] if p2p
+           else sharded(hk, kind, G, am, asg, xm, xsg, P))
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    want = hk.to_host(*hk.matvec(kind, a, sa, x, sx, P))
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    fp.check(kind, am, asg, xm, xsg, *got)

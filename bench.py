@@ -508,7 +508,7 @@ def main():
             "per_unit": f"GS butterfly 1, CT butterfly {C_CT}/{C_GS}, Montgomery product {C_MONT}/{C_GS} "
                         "(minimal integer-pipe clocks relative to GS); full transforms, no pruning credit",
             "vs_microbenchmark": (
-                None if k2_ms <= 0 else
+                None if (world > 1 or k2_ms <= 0) else
                 (cnt["bf_col_fwd"] / MICRO_GS + cnt["bf_col_inv"] / MICRO_CT +
                  cnt["pointwise"] * C_MONT / C_GS / MICRO_GS) / (nsm * sm_max * 1e6) / (k2_ms * 1e-3)),
             "vs_microbenchmark_note": ("K2 time vs its butterflies at the register-resident loop rates of "

@@ -9,7 +9,8 @@
  * Every entry is a multiprecision fixed-point number a = B0 * sum_k B^k a_k with B = 2^64
  * and B0 = 2^-P.  The result is exact (no rounding): y_i = Y_i * 2^-2P.
  *
- * LAYOUT (all arrays row-major, C-contiguous):
+ * LAYOUT (all arrays row-major, C-contiguous; DEVICE magnitude arrays 16-byte aligned -- they are
+ *   staged by 16-byte / TMA bulk copies -- which every cudaMalloc / torch allocation satisfies):
  *   * a vector of `count` numbers is  mag: uint64_t[count][L]  (limb 0 least significant,
  *     L = hk_limbs(P) = ceil(P/64))  plus  sign: int8_t[count]  in {-1, 0, +1};
  *     value = sign * mag * 2^-P.  Inputs must satisfy sign == 0 <=> mag == 0, and every bit >= P

@@ -285,6 +285,7 @@ int run_matvec(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_
                uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream,
                uint32_t stages = HK_STAGE_ALL, bool rounded = false) {
     if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws) return HK_EINVAL;
+    if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;  // 16-byte staging
     Plan pl;
     int rc = make_plan(kind, m, n, P, 0, &pl);
     if (rc) return rc;
@@ -606,6 +607,7 @@ int32_t hk_hankel_shard_forward(int32_t kind, int64_t n, int32_t P, int32_t G, i
                                 const uint64_t *x_mag, const int8_t *x_sign, uint32_t *send,
                                 void *ws, size_t ws_bytes, void *stream) {
     if (!a_mag || !a_sign || !x_mag || !x_sign || !send) return HK_EINVAL;
+    if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
     Plan pl;
     Params prm;
     int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
@@ -638,6 +640,7 @@ int32_t hk_hankel_shard_forward_p2p(int32_t kind, int64_t n, int32_t P, int32_t 
                                     uint32_t *const *recv_ptrs, void *ws, size_t ws_bytes,
                                     void *stream) {
     if (!a_mag || !a_sign || !x_mag || !x_sign || !recv_ptrs) return HK_EINVAL;
+    if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
     Plan pl;
     Params prm;
     int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
@@ -678,7 +681,8 @@ int32_t hk_hankel_shard_finish_p2p(int32_t kind, int64_t n, int32_t P, int32_t G
 
 int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                      const int8_t *a_sign, void *ws, size_t ws_bytes, void *stream) {
-    if (!a_mag || !a_sign || !ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;
+    if (!a_mag || !a_sign || !ws || ((uintptr_t)ws & 255) != 0 || ((uintptr_t)a_mag & 15) != 0)
+        return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
     if (rc) return rc;
@@ -702,7 +706,8 @@ int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64
 int32_t hk_matvec_prepared(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *x_mag,
                            const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *ws,
                            size_t ws_bytes, void *stream) {
-    if (!x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0)
+    if (!x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0 ||
+        ((uintptr_t)x_mag & 15) != 0)
         return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);

@@ -79,6 +79,35 @@ HK_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "mem
 template <int N>  // wait until at most N committed groups are still in flight
 HK_DEV void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// TMA bulk copy (non-tensor) of a contiguous global range into shared memory, completing on an
+// mbarrier (sm_90+ async proxy).  dst / src 16-byte aligned, bytes a multiple of 16.
+HK_DEV void mbar_init(uint64_t *mbar, unsigned count) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+HK_DEV void bulk_copy_g2s(void *dst, const void *src, unsigned bytes, uint64_t *mbar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    const unsigned b = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(b)
+        : "memory");
+}
+HK_DEV void mbar_wait_parity(uint64_t *mbar, unsigned parity) {
+    const unsigned b = (unsigned)__cvta_generic_to_shared(mbar);
+    unsigned done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+            : "=r"(done)
+            : "r"(b), "r"(parity)
+            : "memory");
+    }
+}
+
 // Butterfly with twiddle omega^0 = 1 (GS and CT coincide): no multiplication.
 HK_DEV void bfly1(uint32_t &u, uint32_t &v, uint32_t p) {
     const uint32_t d = subm(u, v, p);

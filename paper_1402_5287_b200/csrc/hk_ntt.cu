@@ -83,6 +83,9 @@ constexpr int k1_row_stride() {  // = 4 (mod 32): transposed [row][sigma] tiles 
 #define HK_K1_MINB 3
 #endif
 constexpr int kK1Rows = HK_K1_ROWS;
+#ifndef HK_K1_TMA
+#define HK_K1_TMA 1  // stage the limb tile with one TMA bulk copy (else per-thread cp.async)
+#endif
 #ifndef HK_K1_L2PF
 #define HK_K1_L2PF 148  // tiles ahead whose limbs are bulk-prefetched into L2 (0: off)
 #endif
@@ -140,7 +143,15 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         const int64_t bytes = nrows * L * 8;
         const char *g = reinterpret_cast<const char *>(mag + r0 * L);
         char *d = reinterpret_cast<char *>(slimb);
+#if HK_K1_TMA
+        // one TMA bulk copy of the tile's contiguous limb block (its 16-byte-aligned part)
+        __shared__ __align__(8) uint64_t s_mbar;
+        if (tid == 0) mbar_init(&s_mbar, 1);
+        __syncthreads();
+        if (tid == 0) bulk_copy_g2s(d, g, (unsigned)(bytes & ~int64_t(15)), &s_mbar);
+#else
         for (int64_t c = tid; c < bytes / 16; c += T) cp_async16(d + 16 * c, g + 16 * c);
+#endif
         if ((bytes & 15) && tid == 0) cp_async8(d + (bytes & ~int64_t(15)), g + (bytes & ~int64_t(15)));
         if (HK_K1_L2PF && tid == 0) {  // bring the limbs of the tile one wave ahead into L2
             const int bt2 = bt + HK_K1_L2PF;
@@ -155,6 +166,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
             }
         }
         cp_async_wait_all();
+#if HK_K1_TMA
+        mbar_wait_parity(&s_mbar, 0);
+#endif
         __syncthreads();
     }
     // ---- validation (A1): bits >= P zero, sign in {-1,0,1}, sign == 0 <=> magnitude == 0;

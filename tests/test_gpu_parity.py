@@ -416,3 +416,21 @@ def test_large_P_slice_transform_2048(hk, kind, n, P):
 def test_planner_limit(hk):
     with pytest.raises(hk.HKError):
         hk.plan(0, 10, 66561)
+
+
+def test_misaligned_magnitudes_rejected(hk):
+    """Magnitude arrays must be 16-byte aligned (16-byte / TMA bulk staging): HK_EINVAL, not a fault."""
+    n, P = 5, 64
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=1)
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    big = torch.empty((2 * n, 1), dtype=torch.int64, device="cuda")
+    a_off = big[1: 2 * n]  # 8-byte offset view
+    a_off.copy_(a)
+    ws = hk.Workspace(0, n, P)
+    y = torch.empty((n, hk.out_limbs(P)), dtype=torch.int64, device="cuda")
+    ys = torch.empty(n, dtype=torch.int8, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    rc = hk._lib.hk_hankel_matvec(n, P, a_off.data_ptr(), sa.data_ptr(), x.data_ptr(), sx.data_ptr(),
+                                  y.data_ptr(), ys.data_ptr(), ws.ptr, ws.nbytes, s)
+    assert rc == hk.HK_EINVAL

@@ -11,6 +11,7 @@
 // runs with the FORWARD roots, which yields the inverse transform with the output index negated
 // (hk_modarith.cuh), so output row i is read from position (N1 - out_off - i) mod N1.
 #pragma once
+#include <type_traits>
 #include "hk_internal.h"
 #include "hk_modarith.cuh"
 
@@ -206,10 +207,16 @@ template <int LOGN1>
 constexpr bool k2_stage_a() { return LOGN1 < 14 || (LOGN1 == 14 && HK_K2_STAGE14); }
 template <int LOGN1>
 constexpr int k2_stage_off() { return (padded_len(1 << LOGN1) + 3) & ~3; }  // 16-byte aligned
+#ifndef HK_K2_SMTW
+#define HK_K2_SMTW 1  // middle / bottom-pass twiddles (table entries < 512) copied into smem
+#endif
+constexpr int kK2LowTw = 512;
+template <int LOGN1>
+constexpr bool k2_smtw() { return HK_K2_SMTW && !k2_stage_a<LOGN1>() && (1 << LOGN1) / 32 >= kK2LowTw / 32; }
 template <int LOGN1>
 constexpr size_t k2_smem_bytes() {
     return k2_stage_a<LOGN1>() ? (size_t)(k2_stage_off<LOGN1>() + (1 << LOGN1)) * 4
-                               : (size_t)padded_len(1 << LOGN1) * 4;
+                               : (size_t)padded_len(1 << LOGN1) * 4 + (k2_smtw<LOGN1>() ? 16 + kK2LowTw * 8 : 0);
 }
 
 template <class TW, int LOGN1, bool SHARD>
@@ -238,11 +245,19 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         }
     }
 
+    // low twiddle levels (h < 512: the middle and bottom passes) in shared memory when enabled
+    using TWM = typename std::conditional<k2_smtw<LOGN1>(), TwShared, TW>::type;
+    const uint2 *twm = twf;
+    if constexpr (k2_smtw<LOGN1>()) {
+        uint2 *tl = reinterpret_cast<uint2 *>(sm + ((padded_len(N1) + 3) & ~3));
+        for (int i = tid; i < kK2LowTw; i += T) tl[i] = __ldg(twf + i);
+        twm = tl;  // visible after the first pass's barrier
+    }
     // ---- X^: forward, bottom pass kept in registers
     {
         const int nx = (int)prm.n;
         k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
-        K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
+        K2DifMiddle<TWM, LOGN1, 1>::run(sm, twm, p);
     }
     uint32_t xr[GPT][GL];
 #pragma unroll
@@ -250,7 +265,7 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         const int g = tid + k * T;
 #pragma unroll
         for (int m = 0; m < GL; ++m) xr[k][m] = sm[pad(g * GL) + m];
-        dif_bottom_regs<TW, RL>(xr[k], twf, p);
+        dif_bottom_regs<TWM, RL>(xr[k], twm, p);
     }
     __syncthreads();
     // ---- A^: forward; bottom pass + pointwise + first inverse pass in registers
@@ -263,7 +278,7 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         } else {
             k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na <= N1 / 2, sm, twf, p);
         }
-        K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
+        K2DifMiddle<TWM, LOGN1, 1>::run(sm, twm, p);
     }
 #pragma unroll
     for (int k = 0; k < GPT; ++k) {
@@ -271,15 +286,15 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
         uint32_t v[GL];
 #pragma unroll
         for (int m = 0; m < GL; ++m) v[m] = sm[pad(g * GL) + m];
-        dif_bottom_regs<TW, RL>(v, twf, p);
+        dif_bottom_regs<TWM, RL>(v, twm, p);
 #pragma unroll
         for (int m = 0; m < GL; ++m) v[m] = mont(v[m], xr[k][m], p, pneg);
-        dit_bottom_regs<TW, RL>(v, twf, p);
+        dit_bottom_regs<TWM, RL>(v, twm, p);
 #pragma unroll
         for (int m = 0; m < GL; ++m) sm[pad(g * GL) + m] = v[m];
     }
     __syncthreads();
-    K2DitMiddle<TW, LOGN1, RL>::run(sm, twf, p);
+    K2DitMiddle<TWM, LOGN1, RL>::run(sm, twm, p);
     const int mrows = (int)prm.m, off = (int)prm.out_off;
     if (!prm.fold) {
         k2_dit_top<TW, LOGN1, T, SHARD>(sm, twf, p, prm, cidx, mrows, off, false);

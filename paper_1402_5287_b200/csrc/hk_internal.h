@@ -12,8 +12,11 @@ constexpr int kNumPrimes = 5;
 constexpr uint64_t kWsMagic = 0x484b5753504c414eull;  // "HKWSPLAN"
 constexpr int kMaxLogN1 = 15;                           // N1 <= 32768 (K2 register budget)
 constexpr int kMinLogN1 = 6;
-constexpr int kSplitLogN1 = 15;
-constexpr int kMaxShards = 8;                           // sigma-coset shards G <= 8                         // K2 as prepare + prepared launches from here
+#ifndef HK_SPLIT_LOGN1
+#define HK_SPLIT_LOGN1 15
+#endif
+constexpr int kSplitLogN1 = HK_SPLIT_LOGN1;             // K2 as prepare + prepared launches from here
+constexpr int kMaxShards = 8;                           // sigma-coset shards G <= 8
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs

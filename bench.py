@@ -357,6 +357,28 @@ def main():
                 "what": "same matvec with the 2-D transform of a prepared once (hk_prepare_a); "
                         "per step: x slicing + transforms, pointwise, inverse, CRT, carry"}
         del A
+        # F1 multi-vector batching: 3 lanes (streams with their own prepared copy), 3 vectors per round
+        LN = 3
+        A = hk.PreparedMatrix(kind, a, sa, P, n, lanes=LN)
+        outs = [(torch.empty((n, plan["Ly"]), dtype=torch.int64, device=dev),
+                 torch.empty((n,), dtype=torch.int8, device=dev)) for _ in range(LN)]
+        for _ in range(W):
+            A.matvec_batch([(x, sx)] * LN, outs=outs, check=False)
+        torch.cuda.synchronize()
+        w0.record(stream)
+        for _ in range(K):
+            A.matvec_batch([(x, sx)] * LN, outs=outs, check=False)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        for lw in A._lane_ws:
+            if lw.status() != hk.HK_OK:
+                raise SystemExit("bench: batched prepared-matvec status not OK")
+        bms = w0.elapsed_time(w1) / (K * LN)
+        warm["batch"] = {"value": 1000.0 / bms, "unit": UNIT, "ms_per_matvec": bms, "lanes": LN,
+                         "what": "PreparedMatrix.matvec_batch: 3 vectors per call over 3 lanes "
+                                 "(CUDA streams, each with its own prepared copy of a's transform); "
+                                 "CUDA events on the calling stream, which waits for every lane"}
+        del A, outs
 
     # ---- secondary: 3 independent problems in flight on 3 streams (kernel tails overlap)
     concurrent = None

@@ -470,7 +470,10 @@ class PreparedMatrix:
     """F1 (fixed-A repeated products, the paper's Lanczos use P:32-36): the 2-D transform of a is
     computed once (hk_prepare_a) and reused by every matvec(x) (hk_matvec_prepared)."""
 
-    def __init__(self, kind, a_mag, a_sign, P, n, m=None, stream=None, check=True):
+    def __init__(self, kind, a_mag, a_sign, P, n, m=None, stream=None, check=True, lanes=1):
+        """lanes > 1: multi-vector batching for matvec_batch() -- that many CUDA streams, each with
+        its own prepared workspace (a's transform computed once per lane), so several vectors'
+        products are in flight at once and fill each other's partial last waves."""
         import torch
         self.kind, self.P, self.n = int(kind), int(P), int(n)
         self.m = self.n if m is None else int(m)
@@ -484,6 +487,22 @@ class PreparedMatrix:
                                  self.ws.nbytes, _stream_ptr(stream)), "hk_prepare_a")
         if check:
             _check(self.ws.status(stream), "hk_prepare_a data status")
+        self.lanes = max(1, int(lanes))
+        self._lane_ws, self._lane_st = [self.ws], [None]
+        if self.lanes > 1:
+            cur = torch.cuda.current_stream() if stream is None else stream
+            for _ in range(self.lanes - 1):
+                st = torch.cuda.Stream(device=a_mag.device)
+                st.wait_stream(cur)
+                ws = Workspace(kind, self.n, P, m=self.m, flags=WS_PREPARED, stream=st)
+                _check(_lib.hk_prepare_a(self.kind, self.m, self.n, self.P, pa, ps, ws.ptr, ws.nbytes,
+                                         st.cuda_stream), "hk_prepare_a")
+                if check:
+                    _check(ws.status(st), "hk_prepare_a data status")
+                self._lane_ws.append(ws)
+                self._lane_st.append(st)
+            self._lane_st[0] = torch.cuda.Stream(device=a_mag.device)
+            self._lane_st[0].wait_stream(cur)
 
     def matvec(self, x_mag, x_sign, out=None, stream=None, check=True):
         import torch
@@ -501,6 +520,42 @@ class PreparedMatrix:
         if check:
             _check(self.ws.status(stream), "hk_matvec_prepared data status")
         return out
+
+    def matvec_batch(self, xs, outs=None, stream=None, check=True):
+        """y_v = A x_v for a list of (x_mag, x_sign) pairs, distributed round-robin over the lanes
+        (see __init__); ordered after and before the calling stream.  Returns the list of outputs."""
+        import torch
+        L, Ly = limbs(self.P), out_limbs(self.P)
+        cur = torch.cuda.current_stream() if stream is None else stream
+        if self.lanes == 1:
+            return [self.matvec(xm, xsg, out=None if outs is None else outs[v], stream=cur, check=check)
+                    for v, (xm, xsg) in enumerate(xs)]
+        for st in self._lane_st:
+            st.wait_stream(cur)
+        res = []
+        for v, (xm, xsg) in enumerate(xs):
+            lane = v % self.lanes
+            st, ws = self._lane_st[lane], self._lane_ws[lane]
+            px = _dev_ptr(xm, _mag_dtypes(), (self.n, L), "x_mag")
+            pxs = _dev_ptr(xsg, (torch.int8,), (self.n,), "x_sign")
+            if outs is None:  # allocated on the calling stream, used on the lane (record_stream below)
+                out = (torch.empty((self.m, Ly), dtype=xm.dtype, device=xm.device),
+                       torch.empty((self.m,), dtype=torch.int8, device=xm.device))
+            else:
+                out = outs[v]
+            py = _dev_ptr(out[0], _mag_dtypes(), (self.m, Ly), "y_mag")
+            pys = _dev_ptr(out[1], (torch.int8,), (self.m,), "y_sign")
+            _check(_lib.hk_matvec_prepared(self.kind, self.m, self.n, self.P, px, pxs, py, pys,
+                                           ws.ptr, ws.nbytes, st.cuda_stream), "hk_matvec_prepared")
+            for t in (xm, xsg, out[0], out[1]):
+                t.record_stream(st)
+            res.append(out)
+        for st in self._lane_st:
+            cur.wait_stream(st)
+        if check:
+            for ws in self._lane_ws:
+                _check(ws.status(cur), "hk_matvec_prepared data status")
+        return res
 
 
 def schoolbook_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, m=None, out=None, stream=None):

@@ -330,6 +330,20 @@ def test_prepared_matrix_many_vectors(hk, kind, n, P):
             fp.check(kind, am, asg, xm, xsg, *got)
 
 
+@pytest.mark.parametrize("kind,n,P,lanes", [(0, 64, 3328, 2), (1, 100, 2000, 3), (2, 77, 700, 2),
+                                            (0, 33, 65, 4)])
+def test_prepared_matrix_batch_lanes(hk, kind, n, P, lanes):
+    """F1 multi-vector batching: vectors spread over lanes (streams with their own prepared copy)."""
+    am, asg, _, _ = gen.make_inputs(kind, n, P, seed=41 + n)
+    A = hk.PreparedMatrix(kind, *hk.to_device(am, asg), P, n, lanes=lanes)
+    xs_host = [gen.uniform(200 + v, 1, n, P) for v in range(2 * lanes + 1)]
+    ys = A.matvec_batch([hk.to_device(xm, xsg) for xm, xsg in xs_host])
+    assert len(ys) == len(xs_host)
+    for v, ((xm, xsg), y) in enumerate(zip(xs_host, ys)):
+        want = oracle.matvec(kind, P, am, asg, xm, xsg)
+        assert_same(hk.to_host(*y), want, f"batch kind={kind} n={n} lanes={lanes} v={v}")
+
+
 def test_prepared_requires_prepare(hk):
     P, n = 128, 10
     am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=3)

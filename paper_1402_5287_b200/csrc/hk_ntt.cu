@@ -340,6 +340,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
 #ifndef HK_K3_BLOCK
 #define HK_K3_BLOCK 320
 #endif
+#ifndef HK_K3_GARNER_SLOT
+#define HK_K3_GARNER_SLOT 1  // Garner slot by slot (CRT words at the residue slot) instead of in pairs
+#endif
 #ifndef HK_K3_MINB
 #define HK_K3_MINB 2
 #endif
@@ -544,6 +547,20 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     }
     // (a) inverse slice NTTs
     K3Dit<LOGN2, 0>::run(sm, prm);
+#if HK_K3_GARNER_SLOT
+    // (b) Garner CRT in place, slot by slot: coefficient s lives at sigma = (N2 - s) mod N2 and its
+    // CRT words overwrite its own residues there, so any thread may take any slot (R N2 slots over
+    // the block: no pairing, no remainder round of pairs)
+    for (int it = tid; it < R * N2; it += T) {
+        const int r = it % R, sg = it / R;
+        uint32_t ra[kNumPrimes], ca[kNumPrimes];
+#pragma unroll
+        for (int kp = 0; kp < kNumPrimes; ++kp) ra[kp] = sm[LY::idx(kp, sg, r)];
+        garner(ra, prm, ca);
+#pragma unroll
+        for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, sg, r)] = ca[k];
+    }
+#else
     // (b) Garner CRT in place: coefficient s lives at sigma = (N2 - s) mod N2 and its CRT words
     // go to sigma = s, so the pair {s, N2 - s} is read and written by one thread.
     for (int it = tid; it < R * (N2 / 2 + 1); it += T) {
@@ -563,6 +580,7 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
             for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, s2, r)] = cb[k];
         }
     }
+#endif
     __syncthreads();
 
     // (c) all R rows at once: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R),
@@ -580,9 +598,14 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
         int sh;
         const int sidx = k3_coef_of_limb(qq, w, &sh);
         if (sidx < 0 || sidx >= S2) return z;
-        const uint64_t C0 = (uint64_t)sm[LY::idx(0, sidx, r)] | ((uint64_t)sm[LY::idx(1, sidx, r)] << 32);
-        const uint64_t C1 = (uint64_t)sm[LY::idx(2, sidx, r)] | ((uint64_t)sm[LY::idx(3, sidx, r)] << 32);
-        const uint32_t w4 = sm[LY::idx(4, sidx, r)];
+#if HK_K3_GARNER_SLOT
+        const int cs = (N2 - sidx) & (N2 - 1);  // CRT words of coefficient sidx sit at its residue slot
+#else
+        const int cs = sidx;
+#endif
+        const uint64_t C0 = (uint64_t)sm[LY::idx(0, cs, r)] | ((uint64_t)sm[LY::idx(1, cs, r)] << 32);
+        const uint64_t C1 = (uint64_t)sm[LY::idx(2, cs, r)] | ((uint64_t)sm[LY::idx(3, cs, r)] << 32);
+        const uint32_t w4 = sm[LY::idx(4, cs, r)];
         const uint64_t C2 = (uint64_t)(int64_t)(int32_t)w4;   // sign-extended bits 128..159
         const uint64_t C3 = (uint64_t)((int64_t)C2 >> 63);      // sign word
         if (sh) {

@@ -343,6 +343,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
 #ifndef HK_K3_GARNER_SLOT
 #define HK_K3_GARNER_SLOT 1  // Garner slot by slot (CRT words at the residue slot) instead of in pairs
 #endif
+#ifndef HK_K3_FLAT_STORE
+#define HK_K3_FLAT_STORE 1  // y rows of a tile stored as one flat range
+#endif
 #ifndef HK_K3_MINB
 #define HK_K3_MINB 2
 #endif
@@ -708,6 +711,44 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
         }
     }
     __syncthreads();
+#if HK_K3_FLAT_STORE
+    if (!prm.round_out) {
+        // the R rows' limbs as one flat range (R Ly / T rounds instead of R ceil(Ly / T)); (rr, l)
+        // advance incrementally (no division; T may exceed Ly for small P)
+        const int nr = (int)(m - r0 < R ? m - r0 : R);
+        const int ndst = prm.p2p ? (1 << prm.shard_gamma) : 1;  // peer memory: every rank's y
+        for (int d = 0; d < ndst; ++d) {
+            uint64_t *ybase = prm.p2p ? prm.peer_ymag[d] : prm.y_mag;
+            int rr = 0, l = tid;
+            while (l >= Ly) { l -= Ly; ++rr; }
+            auto row_ptr = [&](int q) {
+                const int64_t o = r0 + q;
+                return ybase + (prm.reverse_out ? (prm.y_rows - 1 - o) : o) * Ly;
+            };
+            uint64_t *yo = row_ptr(rr);
+            for (; rr < nr;) {
+                yo[l] = ybuf[rr * Ly + l];
+                l += T;
+                if (l >= Ly) {
+                    do { l -= Ly; ++rr; } while (l >= Ly);
+                    yo = row_ptr(rr);
+                }
+            }
+            if (tid < nr) {
+                const int64_t o = r0 + tid;
+                const int64_t orow = prm.reverse_out ? (prm.y_rows - 1 - o) : o;
+                (prm.p2p ? prm.peer_ysign[d] : prm.y_sign)[orow] =
+                    s_neg[tid] ? (int8_t)-1 : (s_zmin[tid] < Ly ? (int8_t)1 : (int8_t)0);
+            }
+        }
+    } else {
+        for (int rr = 0; rr < R && r0 + rr < m; ++rr) {
+            const int64_t o = r0 + rr;
+            k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0,
+                             prm.reverse_out ? (prm.y_rows - 1 - o) : o);
+        }
+    }
+#else
     for (int rr = 0; rr < R; ++rr) {
         const int64_t orow_r = r0 + rr;
         if (orow_r >= m) break;
@@ -725,6 +766,7 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
             k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0, orow);
         }
     }
+#endif
     if (prm.p2p) __threadfence_system();  // peer y stores visible before the next barrier
     (void)row;
 }

@@ -47,6 +47,38 @@ C_GS, C_CT, C_MONT = 8, 9, 10
 BFLY_PER_CLK_SM = 16
 # measured register-resident ceilings (scripts/micro_bfly.cu, profiles/r01/micro_bfly.log)
 MICRO_GS, MICRO_CT = 12.07, 11.22  # butterflies / clk / SM
+# SURVEY.md 8(d) roofline: I_alg = 8 butterflies + 6 pointwise + 15 slice-residues + C_CRT CRT
+# coefficients + C_CARRY carry limbs, against 128 thread-instructions / clk / SM.  The survey's
+# CRT / carry constants (110 / 25) were estimates; C_CRT and C_CARRY are the counts of the
+# current K3's SASS (scripts/k3_sass_counts.py): SASS instructions per
+# Garner coefficient of the CRT loop and per output limb of the carry phase.
+S_BFLY, S_PW, S_RES = 8, 6, 15
+S_CRT_SURVEY, S_CARRY_SURVEY = 110, 25
+C_CRT, C_CARRY = 110, 25
+
+
+def survey_model(plan, m=None):
+    """SURVEY.md 8(d) algorithmic instruction counts per matvec, split by kernel (full
+    transforms, no pruning credit)."""
+    k = plan["k_primes"]
+    N1, N2 = 1 << plan["log_n1"], 1 << plan["log_n2"]
+    lg1, lg2 = plan["log_n1"], plan["log_n2"]
+    rows_a, n = plan["a_count"], plan["n"]
+    m = plan["m"] if m is None else m
+    bf_k1 = k * (rows_a + n) * (N2 // 2) * lg2
+    bf_k2 = 3 * k * N2 * (N1 // 2) * lg1
+    bf_k3 = k * m * (N2 // 2) * lg2
+    pointwise = k * N2 * N1
+    residues = k * (rows_a + n) * plan["Ls"]
+    crt = m * (2 * plan["Ls"] - 1)
+    limbs = m * plan["Ly"]
+    i_k1 = S_BFLY * bf_k1 + S_RES * residues
+    i_k2 = S_BFLY * bf_k2 + S_PW * pointwise
+    i_k3 = S_BFLY * bf_k3 + C_CRT * crt + C_CARRY * limbs
+    i_k3_survey = S_BFLY * bf_k3 + S_CRT_SURVEY * crt + S_CARRY_SURVEY * limbs
+    return dict(butterflies=bf_k1 + bf_k2 + bf_k3, pointwise=pointwise, residues=residues, crt=crt,
+                carry_limbs=limbs, K1=i_k1, K2=i_k2, K3=i_k3, K3_survey_constants=i_k3_survey,
+                total=i_k1 + i_k2 + i_k3)
 
 
 def parse():
@@ -109,6 +141,27 @@ def alg_bytes(plan):
     return io, io + inter
 
 
+def verify_y(kind, am, asg, xm, xsg, y_mag, y_sign, rank, world, dist, dev):
+    """Check of the whole first y before timing: Y mod q of every row against the inputs mod q
+    for three primes q < 2^24 (tests/fingerprint.py: reduction mod q is a ring homomorphism, so it
+    holds at any size).  Rank 0 checks; the verdict is shared with every rank."""
+    ok, why = True, None
+    if rank == 0:
+        from tests import fingerprint as fp
+        ym = y_mag.cpu().numpy().view(np.uint64)
+        ys = y_sign.cpu().numpy()
+        try:
+            fp.check(kind, am, asg, xm, xsg, ym, ys)
+        except AssertionError as e:
+            ok, why = False, str(e)[:200]
+    if world > 1:
+        import torch
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = bool(t.item())
+    return ok, why
+
+
 class ClockSampler:
     """nvidia-smi sampling of SM clocks / throttle reasons during the timed region."""
 
@@ -161,21 +214,39 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(use), "in_timed_region": bool(inside)}
 
 
-def cpu_baseline(wl, rows_per_thread=1):
-    """The oracle as it stands, on a bounded sample of output rows, all host cores."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(wl, min_rows=64, y_gpu=None):
+    """The oracle as it stands, on a bounded sample of output rows (>= 64, a multiple of the core
+    count), all host cores.  With ``y_gpu`` (host copies of the GPU's y) the sampled
+    rows are also compared with the GPU's, limb for limb."""
     import oracle
     kind, n, P = wl["kind"], wl["n"], wl["P"]
     am, asg, xm, xsg = gen.make_inputs(kind, n, P, wl["seed"], wl["recipe"])
     cores = oracle.default_threads()
-    R = min(n, cores * rows_per_thread)
+    R = min(n, -(-min_rows // cores) * cores)
     rows = np.linspace(0, n - 1, R).astype(np.int64)
     t0 = time.perf_counter()
-    oracle.matvec(kind, P, am, asg, xm, xsg, rows=rows, threads=cores)
+    wm, ws_ = oracle.matvec(kind, P, am, asg, xm, xsg, rows=rows, threads=cores)
     dt = time.perf_counter() - t0
-    return {"value": (R / n) / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{R} of {n} output rows of {wl['name']} (each row = n*L^2 = "
-                      f"{n * gen.n_limbs(P) ** 2:.3g} limb products), {dt:.2f} s, extrapolated "
-                      f"to whole matvecs"}
+    out = {"value": (R / n) / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+           "sample": f"{R} of {n} output rows of {wl['name']} (evenly spaced; each row = n*L^2 = "
+                     f"{n * gen.n_limbs(P) ** 2:.3g} limb products), {dt:.2f} s on {cores} threads, "
+                     f"extrapolated to whole matvecs"}
+    if y_gpu is not None:
+        gm, gs = y_gpu
+        bad = int(((gm[rows] != wm).any(axis=1) | (gs[rows] != ws_)).sum())
+        out["gpu_rows_checked"] = R
+        out["gpu_rows_differing"] = bad
+    return out
 
 
 # ---------------------------------------------------------------------------------------------
@@ -235,12 +306,17 @@ def main():
 
     plan = hk.plan(kind, n, P)
     W, K = max(3, args.warmup), args.steps
+    sh_verified_p2p = False
     stage_names = ("K1_slice_rowntt", "K2_column", "K3_finish")
     if world == 1:
         prob = hk.Problem(kind, a, sa, x, sx, P)
         prob.run()
         if prob.status() != hk.HK_OK:
             raise SystemExit("bench: device status not OK")
+        ok, why = verify_y(kind, am, asg, xm, xsg, prob.y_mag, prob.y_sign, 0, 1, None, dev)
+        verification = {"fingerprints_all_rows": ok, "detail": why}
+        if not ok:
+            raise SystemExit(f"bench: y fails its fingerprints ({why})")
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
 
         def step(i=None):
@@ -261,7 +337,18 @@ def main():
         # NCCL all-gather of y; stages: forward, all-to-all, finish + all-gather
         from paper_1402_5287_b200 import dist as hkdist
         sh = hkdist.CosetShardedMatvec(kind, a, sa, x, sx, P)
-        sh.step()
+        sh.step(check=True)
+        ok, why = verify_y(kind, am, asg, xm, xsg, *sh.result(), rank, world, dist, dev)
+        verification = {"fingerprints_all_rows": ok, "p2p_tried": sh.p2p, "detail": why}
+        if not ok and sh.p2p:  # peer-memory exchange gave a wrong y: NCCL exchanges instead
+            sh = hkdist.CosetShardedMatvec(kind, a, sa, x, sx, P, p2p=False)
+            sh.step(check=True)
+            ok, why = verify_y(kind, am, asg, xm, xsg, *sh.result(), rank, world, dist, dev)
+            verification.update(fingerprints_all_rows=ok, fallback="NCCL exchanges after a p2p mismatch",
+                                detail=why)
+        if not ok:
+            raise SystemExit(f"bench: sharded y fails its fingerprints ({why})")
+        sh_verified_p2p = sh.p2p
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
         stage_names = ("shard_forward_K1K2", "all_to_all", "shard_finish_K3+all_gather")
 
@@ -282,7 +369,11 @@ def main():
     else:
         from paper_1402_5287_b200 import dist as hkdist
         sh = hkdist.ShardedHankel(a, sa, x, sx, P)
-        sh.step()
+        sh.step(check=True)
+        ok, why = verify_y(kind, am, asg, xm, xsg, *sh.result(), rank, world, dist, dev)
+        verification = {"fingerprints_all_rows": ok, "detail": why}
+        if not ok:
+            raise SystemExit(f"bench: row-block y fails its fingerprints ({why})")
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
         stage_names = ("-", "shard_compute", "all_gather")
 
@@ -380,9 +471,14 @@ def main():
                                  "CUDA events on the calling stream, which waits for every lane"}
         del A, outs
 
-    # ---- secondary: 3 independent problems in flight on 3 streams (kernel tails overlap)
-    concurrent = None
-    if rank == 0 and world == 1:
+    # ---- throughput mode: a stream of >= 16 independent matvecs with several
+    # in flight; at N = 1 three Problems (own workspaces and y) on three streams, at N > 1 the
+    # sigma-coset CosetStream (3 slots, exchanges on a communication stream).  T = device time of
+    # the whole stream / count (CUDA events on the calling stream, which joins every stream), max
+    # over ranks; the latency-mode headline (one matvec per step) is kept as `value`.
+    throughput = None
+    n_tp = max(16, min(K, 64))
+    if world == 1:
         S_ = 3
         others = [prob]
         for sidx in range(1, S_):
@@ -391,24 +487,54 @@ def main():
             x2, sx2 = hk.to_device(xm2, xsg2, dev)
             others.append(hk.Problem(kind, a2, sa2, x2, sx2, P))
         strs = [torch.cuda.Stream(device=dev) for _ in range(S_)]
+
+        def tp_round(count):
+            for st in strs:
+                st.wait_stream(stream)
+            for t in range(count):
+                others[t % S_].run(stream=strs[t % S_])
+            for st in strs:
+                stream.wait_stream(st)
+
+        tp_round(2 * S_)
         torch.cuda.synchronize()
-        for _ in range(W):
-            for pr, st in zip(others, strs):
-                pr.run(stream=st)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        tp_round(n_tp)
+        c1.record(stream)
         torch.cuda.synchronize()
-        c0 = time.perf_counter()
-        for _ in range(K):
-            for pr, st in zip(others, strs):
-                pr.run(stream=st)
-        torch.cuda.synchronize()
-        cms = (time.perf_counter() - c0) * 1e3 / (K * S_)
+        cms = c0.elapsed_time(c1) / n_tp
         for pr in others:
             if pr.status() != hk.HK_OK:
-                raise SystemExit("bench: concurrent-problem status not OK")
-        concurrent = {"value": 1000.0 / cms, "unit": UNIT, "ms_per_matvec": cms, "problems_in_flight": S_,
-                      "what": "independent C3-shaped problems on separate streams, device-resident inputs; "
-                              "host wall clock over K rounds"}
+                raise SystemExit("bench: throughput-mode status not OK")
+        throughput = {"value": 1000.0 / cms, "unit": UNIT, "ms_per_matvec": cms, "matvecs": n_tp,
+                      "in_flight": S_, "launches": 3 * n_tp,
+                      "what": "stream of independent C3-shaped matvecs, 3 in flight on 3 CUDA streams "
+                              "(own workspaces), device-resident inputs; CUDA events on the calling stream"}
         del others[1:]
+    elif args.plan == "coset":
+        from paper_1402_5287_b200 import dist as hkdist
+        cs = hkdist.CosetStream(kind, (a, sa, x, sx), P, slots=3,
+                                p2p=(getattr(sh, "p2p", False) or "auto") if sh_verified_p2p else False)
+        probs = [(a, sa, x, sx)] * n_tp
+        cs.run(probs[:6])
+        torch.cuda.synchronize()
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        cs.run(probs)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tt = torch.tensor([c0.elapsed_time(c1)], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        cms = float(tt.item()) / n_tp
+        throughput = {"value": 1000.0 / cms, "unit": UNIT, "ms_per_matvec": cms, "matvecs": n_tp,
+                      "in_flight": 3, "p2p": cs.p2p, "launches_per_rank": 3 * n_tp,
+                      "what": "CosetStream: stream of independent matvecs over the sigma-coset shards, 3 slots, "
+                              "exchanges on a communication stream overlapping the next matvec's K1/K2; "
+                              "CUDA events, max over ranks"}
+        del cs
 
     # ---- F4 (secondary): the same matvec with y rounded back to the input format (L+1 limbs)
     rounded = None
@@ -530,8 +656,9 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (K2 column pass): integer-pipe bound
+    # ---- roofline: integer issue slots, 128 thread-instr / clk / SM
     cnt = alg_counts(plan)
+    sm_cnt = survey_model(plan)
     peaks = {}
     if os.path.exists(PEAKS_FILE):
         peaks = json.load(open(PEAKS_FILE))
@@ -539,6 +666,11 @@ def main():
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_bfly = nsm * BFLY_PER_CLK_SM * sm_max * 1e6 / 1e12
     peak_tinstr = nsm * LANES_PER_SM * sm_max * 1e6 / 1e12
+    hbm_peak = float(peaks.get("hbm_gbs", 6549.4))
+    io_bytes, all_bytes = alg_bytes(plan)
+    t_alu = sm_cnt["total"] / (peak_tinstr * 1e12)
+    t_hbm = all_bytes / (hbm_peak * 1e9)
+    t_roof = max(t_alu, t_hbm)
     k2_ms = stage_ms[1]
     traffic = None
     tf = os.path.join(ROOT, "profiles", "k2_traffic.json")
@@ -547,44 +679,55 @@ def main():
             traffic = json.load(open(tf)).get(wl["name"])
         except (ValueError, OSError):
             traffic = None
-    achieved = cnt["k2_bfly_eq"] / (k2_ms * 1e-3) / 1e12 if world == 1 else None
-    ach_instr = cnt["k2_instr"] / (k2_ms * 1e-3) / 1e12 if world == 1 else None
-    io_bytes, all_bytes = alg_bytes(plan)
-    roof = {"bound": "alu", "kernel": "k2_column", "achieved": achieved, "peak": peak_bfly,
-            "unit": "T GS-butterfly-eq/s", "frac": (achieved / peak_bfly) if achieved else None,
+    single = world == 1
+    achieved = sm_cnt["K2"] / (k2_ms * 1e-3) / 1e12 if single else None
+    roof = {"bound": "alu", "kernel": "k2_column", "achieved": achieved, "peak": peak_tinstr,
+            "unit": "T thread-instr/s", "frac": (achieved / peak_tinstr) if achieved else None,
             "traffic": traffic,
-            "peak_source": f"derived: {nsm} SMs x {BFLY_PER_CLK_SM} GS butterflies/clk/SM x {sm_max:.0f} MHz "
-                           "(FMA pipe: IMAD.HI 4 clk + 2 IMAD 2 clk per warp-butterfly per SMSP, "
-                           "scripts/micro_pipes.cu; MEASURED_PEAKS.json sm_max_mhz)",
-            "algorithmic_per_launch": cnt["k2_bfly_eq"],
-            "per_unit": f"GS butterfly 1, CT butterfly {C_CT}/{C_GS}, Montgomery product {C_MONT}/{C_GS} "
-                        "(minimal integer-pipe clocks relative to GS); full transforms, no pruning credit",
-            "vs_microbenchmark": (
-                None if (world > 1 or k2_ms <= 0) else
-                (cnt["bf_col_fwd"] / MICRO_GS + cnt["bf_col_inv"] / MICRO_CT +
-                 cnt["pointwise"] * C_MONT / C_GS / MICRO_GS) / (nsm * sm_max * 1e6) / (k2_ms * 1e-3)),
-            "vs_microbenchmark_note": ("K2 time vs its butterflies at the register-resident loop rates of "
-                                       "scripts/micro_bfly.cu (GS 12.07, CT 11.22 per clk per SM)"),
-            "issue_model": {"achieved": ach_instr, "peak": peak_tinstr, "unit": "Tinstr/s",
-                            "frac": (ach_instr / peak_tinstr) if ach_instr else None,
-                            "per_unit": f"{I_GS}/GS, {I_CT}/CT, {I_MONT}/Montgomery SASS instructions"},
-            "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms_step}
-    if world == 1:  # the same integer-pipe model for the other two kernels (CUDA-event times)
-        roof["other_kernels"] = {
-            name: {"algorithmic_per_launch": cnt[key], "kernel_ms": ms_,
-                   "achieved": cnt[key] / (ms_ * 1e-3) / 1e12,
-                   "frac": cnt[key] / (ms_ * 1e-3) / 1e12 / peak_bfly}
-            for name, key, ms_ in (("k1_slice_rowntt", "k1_bfly_eq", stage_ms[0]),
-                                   ("k3_finish", "k3_bfly_eq", stage_ms[2]))}
-        roof["other_kernels"]["per_unit"] = ("K1: GS butterflies + 2 per slice residue; K3: CT 9/8 + "
-                                             "15 per Garner CRT (GS-butterfly equivalents)")
-    hbm_peak = float(peaks.get("hbm_gbs", 6549.4))
+            "peak_source": f"derived (SURVEY.md 8(d)): {nsm} SMs x {LANES_PER_SM} thread-instr/clk/SM "
+                           f"(4 SMSPs x 32 lanes issue limit) x {sm_max:.0f} MHz (MEASURED_PEAKS.json "
+                           "sm_max_mhz)",
+            "algorithmic_per_launch": sm_cnt["K2"],
+            "per_unit": (f"SURVEY.md 8(d): {S_BFLY} per butterfly, {S_PW} per pointwise product "
+                         "(K2: 3 column NTTs of N1 points per (prime, sigma) column, 5 N2 columns, full "
+                         "transforms, no pruning credit)"),
+            "kernel_ms": k2_ms, "kernel_share_of_step": k2_ms / ms_step,
+            "step_frac": (t_roof / (ms_step * 1e-3)) if single else (t_roof / world) / (ms_step * 1e-3),
+            "step": {"T_roof_us": t_roof * 1e6, "T_alu_us": t_alu * 1e6, "T_hbm_us": t_hbm * 1e6,
+                     "I_alg": sm_cnt["total"], "B_alg": all_bytes, "T_measured_us": ms_step * 1e3,
+                     "definition": "SURVEY.md 8(d): T_roof = max(I_alg / (128 N_SM f), B_alg / HBM peak); "
+                                   "step_frac = T_roof / T_measured (at N > 1: T_roof / N)",
+                     "constants": {"butterfly": S_BFLY, "pointwise": S_PW, "slice_residue": S_RES,
+                                   "crt": C_CRT, "carry_limb": C_CARRY,
+                                   "survey_estimates": {"crt": S_CRT_SURVEY, "carry_limb": S_CARRY_SURVEY}},
+                     "counts": {k_: sm_cnt[k_] for k_ in ("butterflies", "pointwise", "residues", "crt",
+                                                          "carry_limbs")}}}
+    if single:  # the same model per kernel (CUDA-event stage times)
+        roof["kernels"] = {name: {"I_alg": sm_cnt[key], "kernel_ms": ms_,
+                                  "frac": sm_cnt[key] / (peak_tinstr * 1e12) / (ms_ * 1e-3)}
+                           for name, key, ms_ in (("k1_slice_rowntt", "K1", stage_ms[0]),
+                                                  ("k2_column", "K2", stage_ms[1]),
+                                                  ("k3_finish", "K3", stage_ms[2]))}
+        roof["kernels"]["k3_finish"]["frac_survey_constants"] = (
+            sm_cnt["K3_survey_constants"] / (peak_tinstr * 1e12) / (stage_ms[2] * 1e-3))
+        ach_bfly = cnt["k2_bfly_eq"] / (k2_ms * 1e-3) / 1e12
+        roof["pipe_model"] = {
+            "what": "secondary: K2 in GS-butterfly equivalents against the FMA-pipe limit (IMAD.HI 4 clk, "
+                    "IMAD 2 clk per warp per SMSP: GS 8, CT 9, Montgomery 10 pipe clocks)",
+            "achieved": ach_bfly, "peak": peak_bfly, "unit": "T GS-butterfly-eq/s", "frac": ach_bfly / peak_bfly,
+            "vs_microbenchmark": (cnt["bf_col_fwd"] / MICRO_GS + cnt["bf_col_inv"] / MICRO_CT +
+                                  cnt["pointwise"] * C_MONT / C_GS / MICRO_GS) / (nsm * sm_max * 1e6) /
+                                 (k2_ms * 1e-3),
+            "vs_microbenchmark_note": "K2 time vs its butterflies at the register-resident loop rates of "
+                                      "scripts/micro_bfly.cu (GS 12.07, CT 11.22 per clk per SM)"}
     roof["hbm_check"] = {"alg_bytes_per_step": all_bytes,
                          "achieved_gbs": all_bytes / (ms_step * 1e-3) / 1e9, "peak_gbs": hbm_peak}
 
     cb = None
     if not args.no_cpu:
-        cb = cpu_baseline(wl)
+        cb = cpu_baseline(wl, y_gpu=hk.to_host(prob.y_mag, prob.y_sign) if world == 1 else None)
+        if world == 1 and cb["gpu_rows_differing"]:
+            raise SystemExit(f"bench: {cb['gpu_rows_differing']} sampled rows differ from the oracle")
 
     value = 1000.0 / ms_step  # one matvec per step for the whole job
     line = {
@@ -605,11 +748,12 @@ def main():
                          f"{all_bytes / 1e6:.0f} MB traffic) exceeds the 126 MB L2"},
         "stages_ms": dict(zip(stage_names, stage_ms)),
         "roofline": roof,
+        "verification": verification,
         "cpu_baseline": cb,
         "e2e": e2e,
         "warm_a": warm,
         "rounded": rounded,
-        "concurrent": concurrent,
+        "throughput": throughput,
         "gpu_launches": launches_per_step * K,
         "clocks": clocks,
         "library": hk.library_path(),

@@ -182,6 +182,13 @@ class Workspace:
                "hk_workspace_status")
         return int(v.value)
 
+    def status_word(self):
+        """The workspace header's data-status word (int32 at byte 16, include/hk.h) as a 1-element
+        device tensor view, for stream-ordered copies of the status without a host sync."""
+        import torch
+        off = self.ptr - self.buf.data_ptr() + 16
+        return self.buf[off:off + 4].view(torch.int32)
+
 
 def _dev_ptr(t, dtypes, shape, name):
     import torch
@@ -405,6 +412,8 @@ class ShardWorkspace:
         _check(_lib.hk_shard_workspace_init(self.kind, self.n, self.P, self.G, self.ptr, self.nbytes,
                                             _stream_ptr(stream)), "hk_shard_workspace_init")
 
+    status_word = Workspace.status_word
+
     def status(self, stream=None) -> int:
         v = ctypes.c_int32()
         _check(_lib.hk_workspace_status(self.ptr, _stream_ptr(stream), ctypes.byref(v)),
@@ -533,6 +542,9 @@ class PreparedMatrix:
         for st in self._lane_st:
             st.wait_stream(cur)
         res = []
+        # each call resets its lane's status word, so every call's status is copied into its own
+        # device slot right after it, on its lane (checked once at the end)
+        slots = torch.zeros((len(xs),), dtype=torch.int32, device=xs[0][0].device) if check else None
         for v, (xm, xsg) in enumerate(xs):
             lane = v % self.lanes
             st, ws = self._lane_st[lane], self._lane_ws[lane]
@@ -547,14 +559,19 @@ class PreparedMatrix:
             pys = _dev_ptr(out[1], (torch.int8,), (self.m,), "y_sign")
             _check(_lib.hk_matvec_prepared(self.kind, self.m, self.n, self.P, px, pxs, py, pys,
                                            ws.ptr, ws.nbytes, st.cuda_stream), "hk_matvec_prepared")
+            if check:
+                with torch.cuda.stream(st):
+                    slots[v:v + 1].copy_(ws.status_word())
             for t in (xm, xsg, out[0], out[1]):
                 t.record_stream(st)
             res.append(out)
         for st in self._lane_st:
             cur.wait_stream(st)
         if check:
-            for ws in self._lane_ws:
-                _check(ws.status(cur), "hk_matvec_prepared data status")
+            codes = slots.cpu().tolist()  # ordered after every lane (cur waited for them)
+            for v, code in enumerate(codes):
+                if code != HK_OK:
+                    raise HKError(int(code), f"hk_matvec_prepared data status (vector {v})")
         return res
 
 
@@ -605,8 +622,10 @@ def karatsuba_matvec(a_mag, a_sign, x_mag, x_sign, P, cutoff: int = 8, out=None,
     ptr = (buf.data_ptr() + 255) & ~255
     _check(_lib.hk_karatsuba_matvec(n, P, cutoff, *args, ptr, nbytes, _stream_ptr(stream)),
            "hk_karatsuba_matvec")
-    # buf returns to torch's caching allocator, which only reuses it for work ordered after
-    # this call on the same stream
+    # buf goes back to torch's caching allocator when this function returns; it was allocated on
+    # the current stream, so tell the allocator the work on `stream` still uses it
+    if stream is not None:
+        buf.record_stream(stream)
     return out
 
 

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "hk_internal.h"
@@ -157,6 +158,10 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     size_t off = align256(sizeof(WsHeader));
     pl->off_tw = off;
     off = align256(off + (size_t)kNumPrimes * (N1 + N2) * sizeof(uint2));
+    pl->off_negK = off;  // K3 v2 tables, padded by kK3TablePad entries past Ly (no bound checks)
+    off = align256(off + (size_t)(in.Ly + kK3TablePad) * sizeof(uint64_t));
+    pl->off_qmap = off;
+    off = align256(off + (size_t)(in.Ly + 3 + kK3TablePad) * sizeof(uint32_t));
     pl->off_A = off;
     off = align256(off + (size_t)kNumPrimes * N2loc * pl->ldA * 4);
     pl->off_X = off;
@@ -224,6 +229,8 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
     char *base = (char *)ws;
     prm->hdr = (WsHeader *)base;
     prm->tw = (const uint2 *)(base + pl.off_tw);
+    prm->negK = (const uint64_t *)(base + pl.off_negK);
+    prm->qmap = (const uint32_t *)(base + pl.off_qmap);
     prm->Ahat = (uint32_t *)(base + pl.off_A);
     prm->Xhat = (uint32_t *)(base + pl.off_X);
     prm->AT = pl.split_k2 ? (uint32_t *)(base + pl.off_AT) : nullptr;
@@ -263,16 +270,144 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
             prm->gc.inv[j][k] = v;
             prm->gc.inv_q[j][k] = shoup_q(v, kPrimesHost[k]);
         }
+    // K3 v2: ascending prime order (kPrimesHost is descending), H = (M - 1) / 2 mod p_g
+    Garner2Consts &g2 = prm->g2;
+    for (int g = 0; g < kNumPrimes; ++g) {
+        g2.kp[g] = (uint32_t)(kNumPrimes - 1 - g);
+        g2.p[g] = kPrimesHost[g2.kp[g]];
+    }
+    // M = 0 mod p_g, so H = (M - 1) / 2 = -1 / 2 = (p_g - 1) / 2 (mod p_g)
+    for (int g = 0; g < kNumPrimes; ++g) g2.h[g] = (g2.p[g] - 1) / 2;
+    for (int j = 0; j < kNumPrimes; ++j)
+        for (int g = 0; g < kNumPrimes; ++g) {
+            g2.c[j][g] = g2.cq[j][g] = 0;
+            if (j >= g) continue;
+            const uint32_t v = invmod(g2.p[j] % g2.p[g], g2.p[g]);
+            g2.c[j][g] = v;
+            g2.cq[j][g] = shoup_q(v, g2.p[g]);
+        }
+}
+
+// -K mod 2^(64 Ly), K = H sum_{s < S2} 2^(w s), H = (M - 1) / 2 (K3 v2; little-endian u64 limbs)
+std::vector<uint64_t> neg_k_limbs(int32_t w, int32_t S2, int32_t Ly) {
+    Big Mb = big_from(1);
+    for (int k = 0; k < kNumPrimes; ++k) Mb = big_mul(Mb, big_from(kPrimesHost[k]));
+    Big H(Mb.size(), 0);  // (M - 1) / 2: M odd, so shift right by one
+    for (size_t i = 0; i < Mb.size(); ++i) {
+        const uint32_t hi = i + 1 < Mb.size() ? Mb[i + 1] : 0u;
+        H[i] = (Mb[i] >> 1) | (hi << 31);
+    }
+    const size_t NW = (size_t)2 * Ly;  // u32 words of the result
+    std::vector<uint32_t> acc(NW, 0);
+    for (int64_t s = 0; s < S2; ++s) {
+        const int64_t bit = (int64_t)w * s;
+        const int64_t w0 = bit >> 5;
+        const int sh = (int)(bit & 31);
+        if ((size_t)w0 >= NW) break;
+        uint64_t carry = 0;
+        for (size_t i = 0; (size_t)w0 + i < NW; ++i) {
+            const uint64_t lo = i < H.size() ? H[i] : 0u;
+            const uint64_t prev = (i >= 1 && i - 1 < H.size()) ? H[i - 1] : 0u;
+            const uint32_t word = sh ? (uint32_t)((lo << sh) | (prev >> (32 - sh))) : (uint32_t)lo;
+            const uint64_t t = (uint64_t)acc[w0 + i] + word + carry;
+            acc[w0 + i] = (uint32_t)t;
+            carry = t >> 32;
+            if (i > H.size() && carry == 0) break;
+        }
+    }
+    std::vector<uint64_t> out(Ly + kK3TablePad, 0);
+    uint64_t borrow = 1;  // two's complement: ~K + 1 (a carry, despite the name)
+    for (int32_t l = 0; l < Ly; ++l) {
+        const uint64_t v = ~((uint64_t)acc[2 * l] | ((uint64_t)acc[2 * l + 1] << 32));
+        const uint64_t r = v + borrow;
+        borrow = (borrow && r == 0) ? 1 : 0;
+        out[l] = r;
+    }
+    return out;
 }
 
 // Twiddle tables + header (K0), and zeros in the A^ / X^ arrays: their column padding beyond the
 // entry count is never written by K1 and must read as zero in K2 (see ldA / ldX in make_plan).
+// K3 v2 limb -> coefficient map: limb qq holds coefficient s with
+// floor(w s / 64) = qq (w = 65: qq = 65 a + b, s = 64 a + b, b < 64; w = 64: s = qq) shifted by
+// w s mod 64; its CRT words sit at residue slot (N2 - s) mod N2 of K3's shared layout (word offset
+// pad(slot) R for row 0).  Limbs with no coefficient point at slot 1 (s = N2 - 1 >= S2), which K3
+// zeroes.  Entry qq + 3 for qq = -3 .. Ly - 1.
+std::vector<uint32_t> k3_qmap(const hk_plan_info &in) {
+    const int64_t N2 = int64_t(1) << in.log_n2, R = k3_tile_rows(in.log_n2);
+    const int64_t S2 = 2 * (int64_t)in.Ls - 1;
+    auto padw = [](int64_t i) { return i + (i >> 5); };
+    std::vector<uint32_t> q((size_t)in.Ly + 3 + kK3TablePad);
+    for (int64_t qq = -3; qq < in.Ly + kK3TablePad; ++qq) {
+        int64_t slot = 1, sh = 0;
+        if (qq >= 0) {
+            int64_t s = qq, b = 0;
+            if (in.w == 65) { const int64_t a = qq / 65; b = qq - 65 * a; s = 64 * a + b; }
+            if (qq < in.Ly && b < 64 && s < S2) {
+                slot = (N2 - s) & (N2 - 1);
+                sh = in.w == 65 ? b : 0;
+            }
+        }
+        q[(size_t)(qq + 3)] = (uint32_t)((padw(slot) * R) << 6 | sh);
+    }
+    return q;
+}
+
 int init_workspace(const Plan &pl, const Params &prm, void *ws, void *stream) {
     if (cudaMemsetAsync((char *)ws + pl.off_A, 0, pl.off_Y - pl.off_A, (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    // -K table of K3 v2 (pageable source: the copy is staged before cudaMemcpyAsync returns)
+    const std::vector<uint64_t> nk = neg_k_limbs(pl.info.w, 2 * pl.info.Ls - 1, pl.info.Ly);
+    const std::vector<uint32_t> qm = k3_qmap(pl.info);
+    if (cudaMemcpyAsync((char *)ws + pl.off_negK, nk.data(), nk.size() * sizeof(uint64_t),
+                        cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess ||
+        cudaMemcpyAsync((char *)ws + pl.off_qmap, qm.data(), qm.size() * sizeof(uint32_t),
+                        cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
         return HK_ECUDA;
     uint32_t gens[kNumPrimes];
     for (int k = 0; k < kNumPrimes; ++k) gens[k] = primitive_root(kPrimesHost[k]);
     return launch_init(prm, gens, stream);
+}
+
+// Copy streams and events of the synchronous host-buffer call (hk_matvec_host), created once per
+// device and reused across calls (a call takes a context from the pool and returns it before it
+// returns; concurrent calls get distinct contexts).  Host-side handles only: no device memory.
+struct HostCtx {
+    static constexpr int kEvents = 24;
+    int device;
+    cudaStream_t s1, s2;
+    cudaEvent_t ev[kEvents];
+};
+std::mutex g_host_mu;
+std::vector<HostCtx *> g_host_pool;
+
+HostCtx *acquire_host_ctx() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_host_mu);
+        for (size_t i = 0; i < g_host_pool.size(); ++i)
+            if (g_host_pool[i]->device == dev) {
+                HostCtx *c = g_host_pool[i];
+                g_host_pool.erase(g_host_pool.begin() + (long)i);
+                return c;
+            }
+    }
+    HostCtx *c = new HostCtx();
+    c->device = dev;
+    bool ok = cudaStreamCreateWithFlags(&c->s1, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking) == cudaSuccess;
+    for (int i = 0; ok && i < HostCtx::kEvents; ++i)
+        ok = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {
+        delete c;  // handles of a failed creation are leaked rather than destroyed half-made
+        return nullptr;
+    }
+    return c;
+}
+void release_host_ctx(HostCtx *c) {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    g_host_pool.push_back(c);
 }
 
 bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
@@ -430,25 +565,13 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
     // Pipeline (all stream-ordered, host synchronises once at the end):
     //   s1: H2D of x then a in chunks  ->  s0: K1 over the tiles of each chunk as it lands
     //   s0: K2  ->  K3 per chunk of output rows  ->  s2: D2H of that chunk of y
-    cudaStream_t s0 = (cudaStream_t)stream, s1 = nullptr, s2 = nullptr;
-    cudaEvent_t evs[24];
+    cudaStream_t s0 = (cudaStream_t)stream;
+    HostCtx *ctx = acquire_host_ctx();
+    if (!ctx) return HK_ECUDA;
+    cudaStream_t s1 = ctx->s1, s2 = ctx->s2;
     int nev = 0;
-    auto cleanup = [&]() {
-        for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
-        if (s1) cudaStreamDestroy(s1);
-        if (s2) cudaStreamDestroy(s2);
-    };
-    auto new_event = [&]() -> cudaEvent_t {
-        cudaEvent_t e = nullptr;
-        if (nev < 24 && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess)
-            evs[nev++] = e;
-        return e;
-    };
-    if (cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking) != cudaSuccess) {
-        cleanup();
-        return HK_ECUDA;
-    }
+    auto cleanup = [&]() { release_host_ctx(ctx); };
+    auto new_event = [&]() -> cudaEvent_t { return nev < HostCtx::kEvents ? ctx->ev[nev++] : nullptr; };
     char *base = (char *)ws;
     const size_t L = pl.info.L, Ly = pl.info.Ly, na = pl.info.a_count;
     uint64_t *d_am = (uint64_t *)(base + pl.st_amag);
@@ -696,11 +819,10 @@ int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64
         return HK_ECUDA;
     if ((rc = launch_k1_range(prm, stream, 0, k1_tiles_a(prm)))) return rc;
     if ((rc = launch_k2_mode(prm, stream, 1))) return rc;
-    const int32_t one = 1;  // a_ready = 1 (stream-ordered after the transforms)
-    if (cudaMemsetAsync(&prm.hdr->a_ready, 0, sizeof(int32_t), st) != cudaSuccess ||
-        cudaMemsetAsync(&prm.hdr->a_ready, one, 1, st) != cudaSuccess)
-        return HK_ECUDA;
-    return HK_OK;
+    // a_ready = 1 only if a passed validation (stream-ordered after the transforms): a prepare
+    // that saw HK_ERANGE leaves a_ready = 0, so every later hk_matvec_prepared reports HK_EINVAL
+    // instead of computing with a rejected matrix
+    return launch_set_a_ready(prm, stream);
 }
 
 int32_t hk_matvec_prepared(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *x_mag,

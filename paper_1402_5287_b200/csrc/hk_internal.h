@@ -20,6 +20,7 @@ constexpr int kMaxShards = 8;                           // sigma-coset shards G 
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
+constexpr int kK3TablePad = 16;                        // K3 v2 tables: entries past Ly (>= max CH)
 constexpr int kK3MaxLy = 2240;                          // K3 carry: 320 threads, <= 14 limbs per
                                                         // thread over 4 rows / 2 rows (N2 = 2048)
 
@@ -34,6 +35,17 @@ struct GarnerConsts {
     uint32_t inv_q[kNumPrimes][kNumPrimes];  // Shoup quotients
     uint32_t half[kNumPrimes];               // (p_k - 1) / 2: mixed-radix digits of (M-1)/2
     uint32_t M[kNumPrimes];                  // M = p0 p1 p2 p3 p4 as 32-bit words
+};
+
+// K3 v2 CRT: Garner over the primes in ascending order, applied to the
+// residues of C + H (H = (M-1)/2), so the mixed-radix value C'' = C + H in [0, M) is the unsigned
+// coefficient; the carry phase adds -K, K = H sum_{s < S2} 2^(w s) (mod 2^(64 Ly)), once per limb.
+struct Garner2Consts {
+    uint32_t p[kNumPrimes];                  // primes in ascending order (digit order)
+    uint32_t kp[kNumPrimes];                 // index of digit g's prime in PrimeConsts pc[]
+    uint32_t c[kNumPrimes][kNumPrimes];      // p_j^-1 mod p_g (j < g, ascending order)
+    uint32_t cq[kNumPrimes][kNumPrimes];     // Shoup quotients
+    uint32_t h[kNumPrimes];                  // H mod p_g
 };
 
 struct WsHeader {  // first 256 bytes of a workspace
@@ -90,6 +102,10 @@ struct Params {
     int32_t split_k2;            // K2 as MODE 1 (A^ -> AT) + MODE 2 (X^ x AT, inverse) launches
     PrimeConsts pc[kNumPrimes];
     GarnerConsts gc;
+    Garner2Consts g2;
+    const uint64_t *negK;        // Ly limbs of -K mod 2^(64 Ly) (K3 v2), in the workspace
+    const uint32_t *qmap;        // K3 v2: entry qq + 3 (qq = -3 .. Ly - 1) = (smem word offset of
+                                 // the coefficient at limb qq, or of the zero slot) << 6 | shift
 };
 
 struct Plan {
@@ -99,7 +115,7 @@ struct Plan {
     int64_t out_off;
     int32_t reverse_out, x_reversed;
     int64_t ldA, ldX, ldY;
-    size_t off_tw, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
+    size_t off_tw, off_negK, off_qmap, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
     size_t st_amag, st_asign, st_xmag, st_xsign, st_ymag, st_ysign;
     size_t off_AT, off_end_prepared;
     int32_t split_k2;            // N1 >= 2^kSplitLogN1: AT inside the base layout, K2 in two launches
@@ -118,6 +134,10 @@ int launch_k3_range(const Params &prm, void *stream, int64_t row0, int64_t nrows
 // K2 variants: 0 = full (X^ and A^ transforms), 1 = prepare (A^ transform -> AT),
 // 2 = prepared (X^ transform x AT, inverse)
 int launch_k2_mode(const Params &prm, void *stream, int mode);
+// hdr->a_ready = 1 iff hdr->status == HK_OK (end of hk_prepare_a)
+int launch_set_a_ready(const Params &prm, void *stream);
+// rows per K3 tile for a slice-transform length 2^log_n2 (the qmap offsets depend on it)
+int k3_tile_rows(int log_n2);
 // companion (hk_schoolbook.cu)
 int launch_schoolbook(int kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                       const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,

@@ -411,6 +411,52 @@ HK_DEV void garner(const uint32_t r[kNumPrimes], const Params &prm, uint32_t (&c
     cw[0] = a0; cw[1] = a1; cw[2] = a2; cw[3] = a3; cw[4] = a4;
 }
 
+#ifndef HK_K3_V2
+#define HK_K3_V2 1  // unsigned CRT (ascending Garner over C + H) + unsigned carry gather
+#endif
+// K3 v2 CRT: digits of C'' = C + H (H = (M-1)/2, so C'' is in [0, M) with no sign test) with the
+// primes in ascending order p'_0 < ... < p'_4: every earlier digit u_j < p'_j < p'_g, so
+// x = t + p'_g - u_j lies in (0, 2 p'_g) and is = t - u_j (mod p'_g) with no reduction first.
+//   u_g = ((((r_g + h_g) - u_0) c_0g - u_1) c_1g - ...) mod p'_g,   c_jg = p'_j^-1 mod p'_g
+//   C'' = u_0 + p'_0 (u_1 + p'_1 (u_2 + p'_2 (u_3 + p'_3 u_4)))  as five 32-bit words.
+HK_DEV void garner2(const uint32_t r[kNumPrimes], const Params &prm, uint32_t (&cw)[kNumPrimes]) {
+    const Garner2Consts &G = prm.g2;
+    uint32_t u[kNumPrimes];
+#pragma unroll
+    for (int g = 0; g < kNumPrimes; ++g) {
+        const uint32_t p = G.p[g];
+        uint32_t t = addm(r[kNumPrimes - 1 - g], G.h[g], p);  // residues are in descending order
+#pragma unroll
+        for (int j = 0; j < g; ++j) t = red1(shoup(t + p - u[j], G.c[j][g], G.cq[j][g], p), p);
+        u[g] = t;
+    }
+    uint64_t v = (uint64_t)u[4] * G.p[3] + u[3];
+    uint32_t a0 = (uint32_t)v, a1 = (uint32_t)(v >> 32), a2, a3, a4;
+    v = (uint64_t)a0 * G.p[2] + u[2]; a0 = (uint32_t)v;
+    v = (uint64_t)a1 * G.p[2] + (v >> 32); a1 = (uint32_t)v; a2 = (uint32_t)(v >> 32);
+    v = (uint64_t)a0 * G.p[1] + u[1]; a0 = (uint32_t)v;
+    v = (uint64_t)a1 * G.p[1] + (v >> 32); a1 = (uint32_t)v;
+    v = (uint64_t)a2 * G.p[1] + (v >> 32); a2 = (uint32_t)v; a3 = (uint32_t)(v >> 32);
+    v = (uint64_t)a0 * G.p[0] + u[0]; a0 = (uint32_t)v;
+    v = (uint64_t)a1 * G.p[0] + (v >> 32); a1 = (uint32_t)v;
+    v = (uint64_t)a2 * G.p[0] + (v >> 32); a2 = (uint32_t)v;
+    v = (uint64_t)a3 * G.p[0] + (v >> 32); a3 = (uint32_t)v; a4 = (uint32_t)(v >> 32);
+    cw[0] = a0; cw[1] = a1; cw[2] = a2; cw[3] = a3; cw[4] = a4;
+}
+
+// K3 v2 carry helpers: (hi:lo) += (vh:vl) with the carry out counted (add.cc chain), and a
+// branch-free 32-bit select
+HK_DEV void add64_count(uint32_t &lo, uint32_t &hi, int &cnt, uint32_t vl, uint32_t vh) {
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, 0;"
+        : "+r"(lo), "+r"(hi), "+r"(cnt) : "r"(vl), "r"(vh));
+}
+HK_DEV uint32_t sel32(bool c, uint32_t a, uint32_t b) {  // c ? a : b
+    uint32_t d;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+        : "=r"(d) : "r"((uint32_t)c), "r"(a), "r"(b));
+    return d;
+}
+
 constexpr int kK3Block = HK_K3_BLOCK;  // 320: 5 primes x 4 rows x 32 groups = 2 radix-32 groups per thread
 
 // Inverse DIT pass of radix 2^RR at stride S over all (prime, row) transforms of the tile.
@@ -559,7 +605,15 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
         uint32_t ra[kNumPrimes], ca[kNumPrimes];
 #pragma unroll
         for (int kp = 0; kp < kNumPrimes; ++kp) ra[kp] = sm[LY::idx(kp, sg, r)];
+#if HK_K3_V2
+        garner2(ra, prm, ca);
+        if (sg == 1) {  // s = N2 - 1 >= S2 is never a coefficient: a zero slot for the gather
+#pragma unroll
+            for (int k = 0; k < kNumPrimes; ++k) ca[k] = 0;
+        }
+#else
         garner(ra, prm, ca);
+#endif
 #pragma unroll
         for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, sg, r)] = ca[k];
     }
@@ -586,6 +640,110 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
 #endif
     __syncthreads();
 
+#if HK_K3_V2
+    // (c) v2: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R).  Coefficient s
+    // (unsigned C'' < M < 2^155, five words at its residue slot) sits at limb q(s) = floor(w s / 64)
+    // shifted by w s mod 64 (w = 65: s = 64 a + b -> q = 65 a + b, shift b; w = 64: q = s).  The
+    // thread walks positions q = l0 - 3 .. l0 + CH - 1 once, keeping the partial sums of the next
+    // three limbs in registers: limb q is complete after the coefficient at q, and then gets -K's
+    // limb.  u = limb value mod 2^64, e = carries out of those additions (<= 4, added to limb q + 1
+    // below).
+    const int Ly = prm.Ly;
+    const int r = tid % R, k = tid / R, lane_r = lane / R;  // lane_r: position among the row's lanes
+    const int l0 = k * CH;
+    const uint32_t *smr = sm + r;
+    const uint32_t *qmap = prm.qmap + l0;  // entry j: position qq = l0 - 3 + j (padded past Ly)
+    const uint64_t *negk = prm.negK + l0;  // zero-padded past Ly
+    // pending partial sums of limbs q, q + 1, q + 2 as 32-bit halves, and their carry counts
+    uint32_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, a2l = 0, a2h = 0;
+    int n0 = 0, n1 = 0, n2 = 0;
+    uint64_t u[CH];
+    int e[CH];
+#pragma unroll
+    for (int j = 0; j < CH + 3; ++j) {
+        const uint32_t qm = __ldg(qmap + j);
+        const uint32_t o = qm >> 6, sh = qm & 63u;
+        const uint32_t w0 = smr[o], w1 = smr[LY::PS + o], w2 = smr[2 * LY::PS + o],
+                       w3 = smr[3 * LY::PS + o], w4 = smr[4 * LY::PS + o];
+        const uint32_t bs = sh & 31u;
+        const uint32_t h0 = w0 << bs, h1 = __funnelshift_l(w0, w1, bs), h2 = __funnelshift_l(w1, w2, bs),
+                       h3 = __funnelshift_l(w2, w3, bs), h4 = __funnelshift_l(w3, w4, bs),
+                       h5 = __funnelshift_l(w4, 0u, bs);
+        const bool up = sh >= 32u;  // the image starts one 32-bit word higher
+        const uint32_t s0 = sel32(up, 0u, h0), s1 = sel32(up, h0, h1), s2 = sel32(up, h1, h2),
+                       s3 = sel32(up, h2, h3), s4 = sel32(up, h3, h4), s5 = sel32(up, h4, h5),
+                       s6 = sel32(up, h5, 0u);
+        add64_count(a0l, a0h, n0, s0, s1);  // limb q
+        add64_count(a1l, a1h, n1, s2, s3);  // limb q + 1
+        add64_count(a2l, a2h, n2, s4, s5);  // limb q + 2 (s6 -> limb q + 3, below)
+        if (j >= 3) {  // limb l = qq is complete: add -K's limb
+            const uint64_t nk = __ldg(negk + (j - 3));
+            add64_count(a0l, a0h, n0, (uint32_t)nk, (uint32_t)(nk >> 32));
+            u[j - 3] = (uint64_t)a0h << 32 | a0l;
+            e[j - 3] = n0;
+        }
+        a0l = a1l; a0h = a1h; n0 = n1;
+        a1l = a2l; a1h = a2h; n1 = n2;
+        a2l = s6; a2h = 0; n2 = 0;
+    }
+    // the local carry count of the previous chunk's last limb (thread t - R) comes via smem
+    __shared__ int8_t s_ecarry[T];
+    __shared__ int s_neg[R], s_zmin[R];
+    s_ecarry[tid] = (int8_t)e[CH - 1];
+    if (tid < R) { s_neg[tid] = 0; s_zmin[tid] = INT_MAX; }
+    __syncthreads();
+    // binary carry lookahead: w_l = u_l + e_(l-1) generates g_l (carry out) or propagates p_l
+    // (w_l = 2^64 - 1); carry into l + 1 = g_l | (p_l & carry into l).  (G, P) packed as bit 0 / 1.
+    int gp = 2;  // identity: G = 0, P = 1
+    int gbits = 0, pbits = 0;
+    int ein = k > 0 ? (int)s_ecarry[tid - R] : 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const uint64_t uv = u[c] + (uint64_t)ein;
+        const int g = uv < (uint64_t)ein ? 1 : 0;
+        const int pr = uv == ~0ull ? 1 : 0;
+        u[c] = uv;
+        gbits |= g << c;
+        pbits |= pr << c;
+        gp = (g | (pr & gp)) | ((pr & (gp >> 1)) << 1);
+        ein = e[c];
+    }
+    // segmented scan over the chunks of each row (lanes r, r + R, ...): compose(later, earlier)
+    auto gp_compose = [](int later, int earlier) {
+        return ((later | ((later >> 1) & earlier)) & 1) | ((later & earlier) & 2);
+    };
+    int incl = gp;
+#pragma unroll
+    for (int off = R; off < 32; off <<= 1) {
+        const int other = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl = gp_compose(incl, other);
+    }
+    if (lane >= 32 - R) s_wtot[warp * R + (lane - (32 - R))] = incl;  // per (warp, row) total
+    __syncthreads();
+    if (tid < R) {  // carry into each warp's first chunk of row tid
+        int c = 0;
+        for (int wi = 0; wi < T / 32; ++wi) {
+            s_wcarry[wi * R + tid] = c;
+            const int t = s_wtot[wi * R + tid];
+            c = (t & 1) | ((t >> 1) & c);
+        }
+    }
+    __syncthreads();
+    const int prev = __shfl_up_sync(0xffffffffu, incl, R);
+    int carry = s_wcarry[warp * R + r];
+    if (lane_r > 0) carry = (prev & 1) | ((prev >> 1) & carry);
+    int zloc = INT_MAX;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {  // final limbs (mod 2^(64 Ly))
+        const uint64_t v = u[c] + (uint64_t)carry;
+        carry = ((gbits >> c) & 1) | ((pbits >> c) & carry);
+        u[c] = v;
+        if (l0 + c < Ly && v && zloc == INT_MAX) zloc = l0 + c;
+        if (l0 + c == Ly - 1) s_neg[r] = (int)(v >> 63);
+    }
+    if (zloc != INT_MAX) atomicMin(&s_zmin[r], zloc);
+    __syncthreads();  // also: every CRT word has been read, the residue area is free
+#else
     // (c) all R rows at once: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R),
     // so the R rows' words of a coefficient are read by adjacent lanes.
     const int S2 = prm.S2, Ly = prm.Ly, w = prm.w;
@@ -696,6 +854,7 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     }
     if (zloc != INT_MAX) atomicMin(&s_zmin[r], zloc);
     __syncthreads();  // also: every CRT word has been read, the residue area is free
+#endif
     uint64_t *ybuf = reinterpret_cast<uint64_t *>(sm);  // [R][Ly]
     {
         const bool neg = s_neg[r] != 0;
@@ -768,7 +927,6 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     }
 #endif
     if (prm.p2p) __threadfence_system();  // peer y stores visible before the next barrier
-    (void)row;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -896,7 +1054,16 @@ int launch_k2_mode(const Params &prm, void *stream, int mode) {
     }
 }
 
+__global__ void k_set_a_ready(WsHeader *hdr) {
+    if (hdr->magic == kWsMagic) hdr->a_ready = hdr->status == HK_OK ? 1 : 0;
+}
+int launch_set_a_ready(const Params &prm, void *stream) {
+    k_set_a_ready<<<1, 1, 0, (cudaStream_t)stream>>>(prm.hdr);
+    return check_launch();
+}
+
 int k1_tile_rows() { return kK1Rows; }
+int k3_tile_rows(int log_n2) { return log_n2 >= 11 ? 2 : HK_K3_ROWS; }
 int k1_tiles_a(const Params &prm) { return (int)((prm.a_count + kK1Rows - 1) / kK1Rows); }
 int k1_tiles_x(const Params &prm) { return (int)((prm.n + kK1Rows - 1) / kK1Rows); }
 
@@ -923,16 +1090,29 @@ static int launch_k3(const Params &prm, cudaStream_t st, int64_t nrows) {
     return check_launch();
 }
 
+// limbs per thread reachable for a slice length 2^LOGN2 (the planner picks the smallest N2 with
+// 2 ceil(P / w) - 1 <= N2, w in {64, 65}; Ly = 2 ceil(P / 64) + 1 <= kK3MaxLy): only these are built
+template <int LOGN2> constexpr int k3_ch_lo() {
+    return LOGN2 <= 8 ? (LOGN2 == 8 ? 2 : 1) : (LOGN2 == 9 ? 4 : 7);
+}
+template <int LOGN2> constexpr int k3_ch_hi() {
+    return LOGN2 <= 6 ? 1 : (LOGN2 == 7 ? 2 : (LOGN2 == 8 ? 4 : (LOGN2 == 9 ? 7 : 14)));
+}
+template <int LOGN2, int C>
+static int k3_dispatch(const Params &prm, cudaStream_t st, int64_t nrows, int ch) {
+    if constexpr (C > k3_ch_hi<LOGN2>()) {
+        return HK_EUNSUPPORTED;
+    } else {
+        if (ch == C) return launch_k3<LOGN2, C>(prm, st, nrows);
+        return k3_dispatch<LOGN2, C + 1>(prm, st, nrows, ch);
+    }
+}
 template <int LOGN2>
 static int launch_k3_ch(const Params &prm, cudaStream_t st, int64_t nrows) {
     constexpr int TR = kK3Block / k3_rows<LOGN2>();  // threads per row
-    switch ((prm.Ly + TR - 1) / TR) {
-#define HK_CASE(C) case C: return launch_k3<LOGN2, C>(prm, st, nrows);
-        HK_CASE(1) HK_CASE(2) HK_CASE(3) HK_CASE(4) HK_CASE(5) HK_CASE(6) HK_CASE(7)
-        HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12) HK_CASE(13) HK_CASE(14)
-#undef HK_CASE
-        default: return HK_EUNSUPPORTED;
-    }
+    const int ch = (prm.Ly + TR - 1) / TR;
+    if (ch < k3_ch_lo<LOGN2>()) return HK_EUNSUPPORTED;
+    return k3_dispatch<LOGN2, k3_ch_lo<LOGN2>()>(prm, st, nrows, ch);
 }
 
 int launch_k3_range(const Params &prm0, void *stream, int64_t row0, int64_t nrows) {

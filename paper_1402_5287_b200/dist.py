@@ -67,7 +67,9 @@ class ShardedHankel:
         self.blocks = row_blocks(self.n, self.G)
         self.r0, self.nr = self.blocks[self.rank]
         self.nr_max = max(nr for _, nr in self.blocks)
-        self.win = window(a_mag, a_sign, self.r0, self.nr, self.n)
+        # own copies of the window: a view would start r0 L 8 bytes into a_mag, which is only
+        # 8-byte aligned when r0 L is odd, and the C ABI needs 16-byte-aligned magnitudes
+        self.win = tuple(t.clone() for t in window(a_mag, a_sign, self.r0, self.nr, self.n))
         self.x = (x_mag, x_sign)
         self.compute = compute or _cuda_shard
         Ly = 2 * ((P + 63) // 64) + 1
@@ -82,7 +84,12 @@ class ShardedHankel:
         self.y_all = torch.empty((self.G * self.nr_max, Ly), dtype=a_mag.dtype, device=dev)
         self.s_all = torch.empty((self.G * self.nr_max,), dtype=torch.int8, device=dev)
 
-    def step(self):
+    def check_status(self):
+        """MIN all-reduce of every rank's data status (HK_OK = 0, errors < 0): raises HKError on
+        every rank if any rank's inputs were rejected (its y rows are then unspecified)."""
+        _agree_status(self.dist, self.group, self.ws, self.x[0].device)
+
+    def step(self, check=False):
         if self.nr > 0:
             kw = {"ws": self.ws} if self.ws is not None else {}
             out = (self.y_loc[: self.nr], self.s_loc[: self.nr])
@@ -91,6 +98,8 @@ class ShardedHankel:
             if ym.data_ptr() != self.y_loc.data_ptr():
                 self.y_loc[: self.nr].copy_(ym)
                 self.s_loc[: self.nr].copy_(ys)
+        if check:
+            self.check_status()
         self._gather()
         return self.result()
 
@@ -114,9 +123,20 @@ class ShardedHankel:
         return self.y_all.index_select(0, it), self.s_all.index_select(0, it)
 
 
-def hankel_matvec(a_mag, a_sign, x_mag, x_sign, P, group=None, compute=None):
+def _agree_status(dist, group, ws, device):
+    import torch
+    from . import HK_OK, HKError
+    code = ws.status() if ws is not None else HK_OK
+    t = torch.tensor([code], dtype=torch.int32, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    worst = int(t.item())
+    if worst != HK_OK:
+        raise HKError(worst, "sharded matvec data status (MIN over ranks)")
+
+
+def hankel_matvec(a_mag, a_sign, x_mag, x_sign, P, group=None, compute=None, check=True):
     """y = A_H x sharded by rows over the process group; returns the full y on every rank."""
-    return ShardedHankel(a_mag, a_sign, x_mag, x_sign, P, group=group, compute=compute).step()
+    return ShardedHankel(a_mag, a_sign, x_mag, x_sign, P, group=group, compute=compute).step(check)
 
 
 # ---------------------------------------------------------------------------------------------
@@ -255,14 +275,130 @@ class CosetShardedMatvec:
             return self.y_pad[self.y_rows - self.n:], self.s_pad[self.y_rows - self.n:]
         return self.y_pad[: self.n], self.s_pad[: self.n]
 
-    def step(self):
+    def check_status(self):
+        """MIN all-reduce of every rank's data status; raises HKError on every rank if any rank's
+        K1 rejected its inputs."""
+        _agree_status(self.dist, self.group, self.ws, self.inputs[0].device)
+
+    def step(self, check=False):
         self.compute_forward()
+        if check:
+            self.check_status()
         self.exchange()
         self.compute_finish()
         self.gather()
         return self.result()
 
 
-def coset_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, group=None):
+def coset_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, group=None, check=True):
     """y = A x over the process group with plan P-2; returns the full y on every rank."""
-    return CosetShardedMatvec(kind, a_mag, a_sign, x_mag, x_sign, P, group=group).step()
+    return CosetShardedMatvec(kind, a_mag, a_sign, x_mag, x_sign, P, group=group).step(check)
+
+
+class CosetStream:
+    """Throughput mode of plan P-2 (the multi-GPU rate of a stream of independent
+    matvecs, the paper's repeated-product use P:32-36).  ``slots`` CosetShardedMatvec
+    instances (each with its own workspace, exchange buffers and padded y) are used round-robin.
+    On CUDA the exchanges -- the all-to-all (or, with peer memory, the device barrier that ends
+    the fused K2 stores) and the y all-gather (or the barrier after K3's fused stores) -- are
+    enqueued on a communication stream, so matvec t's exchanges overlap the K1/K2 of matvec t+1
+    and the K3 of matvec t-1 on the compute stream.  The collectives are issued in the same
+    order on every rank (X0, X1, G0, X2, G1, ...), which NCCL requires.
+
+    Slot reuse: matvec t (slot t mod S) starts only after the y all-gather of matvec t - S has
+    completed on this rank; that all-gather (NCCL) or barrier (peer memory) also proves every
+    rank finished reading its receive buffer of that slot, so K2's stores of matvec t -- local or
+    into peers -- cannot overwrite data still in use.  With peer memory and a ``consume``
+    callback, one more barrier after ``consume`` keeps other ranks' K3 stores of matvec t + S out
+    of this rank's y until it has been consumed.
+
+    The CPU (gloo) path runs the same sequence synchronously, for the tests."""
+
+    def __init__(self, kind, inputs_like, P, slots=3, group=None, forward=None, finish=None,
+                 info=None, p2p="auto"):
+        import torch
+        self.slots = [CosetShardedMatvec(kind, *inputs_like, P, group=group, forward=forward,
+                                         finish=finish, info=info, p2p=p2p) for _ in range(slots)]
+        self.S = len(self.slots)
+        self.cuda = inputs_like[0].is_cuda
+        self.p2p = self.slots[0].p2p
+        self.comp = self.comm = None
+        if self.cuda:
+            self.comp = torch.cuda.current_stream()
+            self.comm = torch.cuda.Stream(device=inputs_like[0].device)
+            ev = lambda: [torch.cuda.Event() for _ in range(self.S)]  # noqa: E731
+            self.ev_fwd, self.ev_x, self.ev_fin, self.ev_done = ev(), ev(), ev(), ev()
+
+    def _stream(self, s):
+        import contextlib
+        import torch
+        return torch.cuda.stream(s) if self.cuda else contextlib.nullcontext()
+
+    def run(self, problems, consume=None, check=False):
+        """Runs y_t = A_t x_t for every (a_mag, a_sign, x_mag, x_sign) in ``problems``; calls
+        ``consume(t, y_mag, y_sign)`` (on the communication stream when CUDA) once y_t is complete
+        on this rank -- the views stay valid only until slot t mod S is reused.  ``check``: the
+        data status of every matvec is captured on the device and MIN-all-reduced at the end
+        (HKError on every rank if any rank rejected an input).  Returns the number of matvecs."""
+        import torch
+        S, used = self.S, [False] * self.S
+        statuses = []
+
+        def finish(t):
+            s = t % S
+            sl = self.slots[s]
+            with self._stream(self.comp):
+                if self.cuda:
+                    self.comp.wait_event(self.ev_x[s])
+                sl.compute_finish()
+                if self.cuda:
+                    self.ev_fin[s].record(self.comp)
+            with self._stream(self.comm):
+                if self.cuda:
+                    self.comm.wait_event(self.ev_fin[s])
+                sl.gather()
+                if consume is not None:
+                    consume(t, *sl.result())
+                    if self.p2p:
+                        sl.h_y.barrier()
+                if self.cuda:
+                    self.ev_done[s].record(self.comm)
+
+        count = 0
+        for t, prob in enumerate(problems):
+            s = t % S
+            sl = self.slots[s]
+            with self._stream(self.comp):
+                if self.cuda and used[s]:
+                    self.comp.wait_event(self.ev_done[s])
+                sl.inputs = tuple(prob)
+                sl.compute_forward()
+                if check and sl.ws is not None:
+                    w = torch.empty((1,), dtype=torch.int32, device=prob[0].device)
+                    w.copy_(sl.ws.status_word())
+                    statuses.append(w)
+                if self.cuda:
+                    self.ev_fwd[s].record(self.comp)
+            used[s] = True
+            with self._stream(self.comm):
+                if self.cuda:
+                    self.comm.wait_event(self.ev_fwd[s])
+                sl.exchange()
+                if self.cuda:
+                    self.ev_x[s].record(self.comm)
+            if t >= 1:
+                finish(t - 1)
+            count += 1
+        if count:
+            finish(count - 1)
+        if self.cuda:
+            self.comp.wait_stream(self.comm)
+        if check:
+            from . import HK_OK, HKError
+            worst = torch.stack(statuses).min().reshape(1) if statuses else torch.zeros(
+                (1,), dtype=torch.int32, device=self.slots[0].inputs[0].device)
+            sl = self.slots[0]
+            sl.dist.all_reduce(worst, op=sl.dist.ReduceOp.MIN, group=sl.group)
+            if int(worst.item()) != HK_OK:
+                raise HKError(int(worst.item()), "coset stream data status (MIN over ranks)")
+        return count

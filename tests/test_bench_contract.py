@@ -36,7 +36,12 @@ def test_cuda_arm_line():
     roof = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in roof
-    assert roof["bound"] == "alu" and 0 < roof["frac"] < 1
+    assert roof["bound"] == "alu" and 0 < roof["frac"] < 1 and 0 < roof["step_frac"] < 1
+    assert set(roof["kernels"]) == {"k1_slice_rowntt", "k2_column", "k3_finish"}
+    assert d["verification"]["fingerprints_all_rows"] is True
+    assert d["cpu_baseline"] is None or d["cpu_baseline"]["gpu_rows_differing"] == 0
+    tp = d["throughput"]
+    assert tp["value"] > 0 and tp["matvecs"] >= 16
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] == 3 * d["steps"]

@@ -155,3 +155,128 @@ def test_coset_exchange_gloo_world2(kind, n, P):
             assert last == 1000 + world - 1 and first == 1000 + (yr - n) // rpr
         else:
             assert first == 1000 and last == 1000 + (n - 1) // rpr
+
+
+# ---------------------------------------------------------------------------------------------
+# throughput mode (CosetStream): a stream of independent matvecs over S slots.  Stand-in phases
+# tag every word with the problem id, so the test pins that each consumed y holds the blocks of
+# its own problem from every rank, in order, across slot reuse.
+def _stream_worker(rank, world, port, kind, n, P, nprob, slots, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1402_5287_b200 as hk
+        from paper_1402_5287_b200 import dist as hd
+        info = hk.shard_plan(kind, n, P, world)
+        chunk, rpr = info["chunk_words"], info["rows_per_rank"]
+
+        def forward(ws, g, am, asg, xm, xsg, send):
+            pid = int(am[0, 0])
+            for dst in range(world):
+                send[dst * chunk:(dst + 1) * chunk] = pid * 100 + g * 10 + dst
+
+        def finish(ws, g, recv, y_mag, y_sign):
+            pids = {int(recv[src * chunk]) // 100 for src in range(world)}
+            assert len(pids) == 1, pids  # every source rank's chunk is from the same problem
+            routed = [int(recv[src * chunk]) % 100 for src in range(world)]
+            assert routed == [src * 10 + g for src in range(world)], routed
+            y_mag[g * rpr:(g + 1) * rpr] = pids.pop() * 1000 + g
+
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=1)
+        base = [torch.from_numpy(am.view(np.int64)), torch.from_numpy(asg),
+                torch.from_numpy(xm.view(np.int64)), torch.from_numpy(xsg)]
+        probs = []
+        for t in range(nprob):
+            a_t = base[0].clone()
+            a_t[0, 0] = 7 + t  # problem id
+            probs.append((a_t, base[1], base[2], base[3]))
+        got = []
+
+        def consume(t, ym, ys):
+            got.append((t, [int(ym[0, 0]), int(ym[-1, 0])],
+                        sorted({int(v) for v in sh.slots[t % slots].y_pad[:, 0]})))
+
+        sh = hd.CosetStream(kind, base, P, slots=slots, forward=forward, finish=finish, info=info)
+        cnt = sh.run(probs, consume=consume)
+        q.put((rank, cnt, got, rpr, info["y_rows"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,slots", [(0, 3), (1, 2), (2, 3)])
+def test_coset_stream_gloo_world2(kind, slots):
+    import paper_1402_5287_b200 as hk
+    world, n, P, nprob = 2, 64, 4200, 7
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stream_worker, args=(r, world, port, kind, n, P, nprob, slots, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, cnt, got, rpr, yr in res:
+        assert cnt == nprob and [t for t, _, _ in got] == list(range(nprob))
+        for t, _, vals in got:
+            pid = 7 + t
+            assert vals == [pid * 1000 + g for g in range(world)], (t, vals)
+
+
+# ---------------------------------------------------------------------------------------------
+# peer-memory set-up agreement: a rank that cannot allocate symmetric memory makes every rank
+# fall back to the NCCL exchanges (MIN all-reduce), without a rank entering the rendezvous alone
+def _p2p_fallback_worker(rank, world, port, fail_rank, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+        import paper_1402_5287_b200 as hk
+        from paper_1402_5287_b200 import dist as hd
+        kind, n, P = 0, 64, 4200
+        info = hk.shard_plan(kind, n, P, world)
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=1)
+        t = [torch.from_numpy(am.view(np.int64)), torch.from_numpy(asg),
+             torch.from_numpy(xm.view(np.int64)), torch.from_numpy(xsg)]
+        sh = hd.CosetShardedMatvec(kind, *t, P, forward=lambda *a: None, finish=lambda *a: None,
+                                   info=info)
+        calls = []
+        if rank == fail_rank:
+            def empty(*a, **k):
+                raise RuntimeError("no symmetric memory here")
+        else:
+            def empty(*shape, dtype=None, device=None):
+                return torch.zeros(shape, dtype=dtype)
+        orig_e, orig_r = symm_mem.empty, symm_mem.rendezvous
+        symm_mem.empty = empty
+        symm_mem.rendezvous = lambda *a, **k: calls.append(1)
+        try:
+            ok = sh._setup_p2p(info["buffer_words"], info["y_rows"], 9, torch.int64,
+                               torch.device("cpu"))
+        finally:
+            symm_mem.empty, symm_mem.rendezvous = orig_e, orig_r
+        q.put((rank, ok, len(calls)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [0, 1])
+def test_p2p_setup_falls_back_together(fail_rank):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_fallback_worker, args=(r, world, port, fail_rank, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok, rendezvous_calls in res:
+        assert ok is False and rendezvous_calls == 0

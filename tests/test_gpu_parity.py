@@ -255,13 +255,24 @@ def _sampled(hk, name, rows_extra=()):
 
 
 def test_c2_full_oracle(hk):
+    """BASELINE configs[1] in full: every row against a live oracle run (and the fingerprints)."""
     c = gen.CONFIGS["C2"]
     am, asg, xm, xsg = gen.config_inputs("C2")
     got = run_gpu(hk, 0, am, asg, xm, xsg, c["P"])
     fp.check(0, am, asg, xm, xsg, *got)
-    rows = np.arange(0, 1024, 16)
-    wm, ws_ = oracle.matvec(0, c["P"], am, asg, xm, xsg, rows=rows)
-    assert_same((got[0][rows], got[1][rows]), (wm, ws_), "C2 rows")
+    assert_same(got, oracle.matvec(0, c["P"], am, asg, xm, xsg), "C2 all rows")
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("P", [64, 200])
+def test_n1_2p14_all_rows(hk, kind, P):
+    """n = 8000: the N1 = 2^14 column kernel C3 runs (256-thread K2, 2 CTAs/SM, shared-memory
+    twiddles), at a small P so the oracle finishes every row in seconds."""
+    full_case(hk, kind, 8000, P, seed=8000 + P + kind)
+
+
+def test_n1_2p14_all_rows_n2_128(hk):
+    full_case(hk, 0, 8000, 2100, seed=82100)  # Ls = 33, N2 = 128
 
 
 @pytest.mark.parametrize("name", ["C3", "C4", "C5T", "C5C"])
@@ -448,3 +459,69 @@ def test_misaligned_magnitudes_rejected(hk):
     rc = hk._lib.hk_hankel_matvec(n, P, a_off.data_ptr(), sa.data_ptr(), x.data_ptr(), sx.data_ptr(),
                                   y.data_ptr(), ys.data_ptr(), ws.ptr, ws.nbytes, s)
     assert rc == hk.HK_EINVAL
+
+
+# ---------------------------------------------------------------------------------------------
+# round-2 hazards: data status across prepared / batched calls, shard alignment
+def test_prepare_with_rejected_a_poisons_later_calls(hk):
+    """hk_prepare_a on an a with a bit >= P: a_ready stays 0, so every later prepared matvec
+    reports an error instead of computing with the rejected matrix."""
+    n, P = 30, 300
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=9)
+    am = am.copy()
+    am[4, -1] |= np.uint64(1) << np.uint64(63)
+    A = hk.PreparedMatrix(0, *hk.to_device(am, asg), P, n, check=False)
+    assert A.ws.status() == hk.HK_ERANGE
+    for _ in range(2):
+        with pytest.raises(hk.HKError):
+            A.matvec(*hk.to_device(xm, xsg))
+
+
+def test_matvec_batch_reports_each_vectors_status(hk):
+    """More vectors than lanes: a rejected x in an early round is reported even though later
+    calls on the same lane reset the lane's status word."""
+    n, P, lanes = 40, 500, 2
+    am, asg, _, _ = gen.make_inputs(0, n, P, seed=10)
+    A = hk.PreparedMatrix(0, *hk.to_device(am, asg), P, n, lanes=lanes)
+    xs = [gen.uniform(300 + v, 1, n, P) for v in range(2 * lanes + 1)]
+    bad = 1
+    xm_bad = xs[bad][0].copy()
+    xm_bad[0, -1] |= np.uint64(1) << np.uint64(62)
+    xs[bad] = (xm_bad, xs[bad][1])
+    with pytest.raises(hk.HKError, match=f"vector {bad}"):
+        A.matvec_batch([hk.to_device(xm, xsg) for xm, xsg in xs])
+    ys = A.matvec_batch([hk.to_device(xm, xsg) for xm, xsg in xs[2:]])  # the others are fine
+    for (xm, xsg), y in zip(xs[2:], ys):
+        assert_same(hk.to_host(*y), oracle.matvec(0, P, am, asg, xm, xsg), "batch after error")
+
+
+def test_rowblock_window_alignment(hk):
+    """A row-block window starting r0 L 8 bytes into a_mag is only 8-byte aligned when r0 L is odd;
+    the C ABI rejects it (HK_EINVAL) and dist.ShardedHankel therefore uses its own copy."""
+    from paper_1402_5287_b200 import dist as hkdist
+    n, P = 50, 3 * 64 - 5  # L = 3 (odd)
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=11)
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    r0, nr = 7, 20  # r0 L = 21: odd
+    wm, wsg = hkdist.window(a, sa, r0, nr, n)
+    with pytest.raises(hk.HKError):
+        hk.hankel_rect_matvec(wm, wsg, x, sx, P, nr)
+    got = hk.hankel_rect_matvec(wm.clone(), wsg.clone(), x, sx, P, nr)
+    want = oracle.matvec(0, P, am, asg, xm, xsg, rows=np.arange(r0, r0 + nr))
+    assert_same(hk.to_host(*got), want, "aligned window copy")
+
+
+def test_circulant_w64_plan(hk):
+    """Circulant n = 32768 (cyclic N1 = 2^15), P = 33,216: the capacity bound rules out w = 65, so
+    the planner takes w = 64, N2 = 2048 (K3 with 2-row tiles).  Fingerprints of every row and
+    three rows against the oracle."""
+    n, P = 32768, 33216
+    pl = hk.plan(2, n, P)
+    assert pl["w"] == 64 and pl["log_n2"] == 11 and pl["cyclic"] == 1
+    am, asg, xm, xsg = gen.make_inputs(2, n, P, seed=64)
+    gm, gs = run_gpu(hk, 2, am, asg, xm, xsg, P)
+    fp.check(2, am, asg, xm, xsg, gm, gs)
+    rows = np.array([0, 12345, n - 1])
+    wm, ws_ = oracle.matvec(2, P, am, asg, xm, xsg, rows=rows)
+    assert_same((gm[rows], gs[rows]), (wm, ws_), "w=64 circulant rows")

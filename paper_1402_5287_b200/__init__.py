@@ -474,6 +474,10 @@ class Problem:
     def status(self, stream=None) -> int:
         return self.ws.status(stream)
 
+    def result(self):
+        """(y_mag, y_sign) device tensors of the last run (overwritten by the next)."""
+        return self.y_mag, self.y_sign
+
 
 class PreparedMatrix:
     """F1 (fixed-A repeated products, the paper's Lanczos use P:32-36): the 2-D transform of a is

@@ -20,7 +20,7 @@ constexpr int kMaxShards = 8;                           // sigma-coset shards G 
 constexpr int kMaxLogN2 = 11;                           // N2 <= 2048 -> Ls <= 1024
 constexpr int kMinLogN2 = 5;
 constexpr int kMaxW = 65;                               // a slice spans at most two limbs
-constexpr int kK3TablePad = 16;                        // K3 v2 tables: entries past Ly (>= max CH)
+constexpr int kK3TablePad = 176;  // K3 v2 tables: entries past Ly (> threads per row, 160, + max CH)
 constexpr int kK3MaxLy = 2240;                          // K3 carry: 320 threads, <= 14 limbs per
                                                         // thread over 4 rows / 2 rows (N2 = 2048)
 

@@ -351,6 +351,12 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
 #endif
 template <int LOGN2>
 constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : HK_K3_ROWS; }
+// threads per K3 CTA and CTAs per SM: 80 threads per row of the tile (320 for the 2-row tiles of
+// N2 = 2048, HK_K3_BLOCK otherwise)
+template <int LOGN2>
+constexpr int k3_threads() { return LOGN2 >= 11 ? 320 : HK_K3_BLOCK; }
+template <int LOGN2>
+constexpr int k3_minb() { return LOGN2 >= 11 ? 2 : HK_K3_MINB; }
 
 template <int LOGN2>
 struct K3Layout {
@@ -457,7 +463,6 @@ HK_DEV uint32_t sel32(bool c, uint32_t a, uint32_t b) {  // c ? a : b
     return d;
 }
 
-constexpr int kK3Block = HK_K3_BLOCK;  // 320: 5 primes x 4 rows x 32 groups = 2 radix-32 groups per thread
 
 // Inverse DIT pass of radix 2^RR at stride S over all (prime, row) transforms of the tile.
 template <int LOGN2, int RR, int S>
@@ -465,7 +470,7 @@ HK_DEV void k3_dit_pass(uint32_t *sm, const Params &prm) {
     using LY = K3Layout<LOGN2>;
     constexpr int N = 1 << LOGN2, G = 1 << RR, NG = N / G, R = LY::R;
     constexpr int total = kNumPrimes * R * NG;
-    for (int gi = threadIdx.x; gi < total; gi += kK3Block) {
+    for (int gi = threadIdx.x; gi < total; gi += k3_threads<LOGN2>()) {
         const int r = gi % R, rest = gi / R;
         const int g = rest % NG, kp = rest / NG;
         const uint32_t p = prm.pc[kp].p;
@@ -558,10 +563,10 @@ HK_DEV void k3_store_rounded(const Params &prm, const uint64_t *M, bool neg, int
     __syncthreads();  // s_first reuse
 }
 
-template <int LOGN2, int CH>  // CH = limbs per thread = ceil(Ly / (kK3Block / R))
-__global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
+template <int LOGN2, int CH>  // CH = limbs per thread = ceil(Ly / (k3_threads / R))
+__global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_finish(Params prm) {
     using LY = K3Layout<LOGN2>;
-    constexpr int N2 = 1 << LOGN2, R = LY::R, T = kK3Block;
+    constexpr int N2 = 1 << LOGN2, R = LY::R, T = k3_threads<LOGN2>();
     extern __shared__ uint32_t sm[];  // residues -> CRT words [5][N2][R] (swizzled) -> y rows [R][Ly]
     __shared__ int s_wtot[T / 32 * R], s_wcarry[T / 32 * R];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -657,8 +662,15 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     // pending partial sums of limbs q, q + 1, q + 2 as 32-bit halves, and their carry counts
     uint32_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, a2l = 0, a2h = 0;
     int n0 = 0, n1 = 0, n2 = 0;
+    // Limb c of the chunk: v_c = its sum mod 2^64, e_c = carries out of that sum (<= 4).  Binary
+    // lookahead on w_c = v_c + e_(c-1): w_c generates g_c (carry out) or propagates p_c
+    // (w_c = 2^64 - 1); carry into c + 1 = g_c | (p_c & carry into c).  For c >= 1 e_(c-1) is this
+    // thread's, so w_c, g_c, p_c are formed here; limb 0 waits for the previous chunk's e.
     uint64_t u[CH];
-    int e[CH];
+    uint32_t v0l = 0, v0h = 0;       // limb 0 before e_in
+    int e_prev = 0;
+    uint32_t gbits = 0, pbits = 0;
+    uint32_t Gt = 0, Pt = 1;         // (G, P) of limbs 1 .. c
 #pragma unroll
     for (int j = 0; j < CH + 3; ++j) {
         const uint32_t qm = __ldg(qmap + j);
@@ -677,10 +689,22 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
         add64_count(a1l, a1h, n1, s2, s3);  // limb q + 1
         add64_count(a2l, a2h, n2, s4, s5);  // limb q + 2 (s6 -> limb q + 3, below)
         if (j >= 3) {  // limb l = qq is complete: add -K's limb
-            const uint64_t nk = __ldg(negk + (j - 3));
+            const int c = j - 3;
+            const uint64_t nk = __ldg(negk + c);
             add64_count(a0l, a0h, n0, (uint32_t)nk, (uint32_t)(nk >> 32));
-            u[j - 3] = (uint64_t)a0h << 32 | a0l;
-            e[j - 3] = n0;
+            if (c == 0) {
+                v0l = a0l; v0h = a0h;
+            } else {
+                int g = 0;
+                add64_count(a0l, a0h, g, (uint32_t)e_prev, 0u);
+                const uint32_t pr = (a0l & a0h) == 0xffffffffu;
+                u[c] = (uint64_t)a0h << 32 | a0l;
+                gbits |= (uint32_t)g << c;
+                pbits |= pr << c;
+                Gt = (uint32_t)g | (pr & Gt);
+                Pt &= pr;
+            }
+            e_prev = n0;
         }
         a0l = a1l; a0h = a1h; n0 = n1;
         a1l = a2l; a1h = a2h; n1 = n2;
@@ -689,25 +713,20 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     // the local carry count of the previous chunk's last limb (thread t - R) comes via smem
     __shared__ int8_t s_ecarry[T];
     __shared__ int s_neg[R], s_zmin[R];
-    s_ecarry[tid] = (int8_t)e[CH - 1];
+    s_ecarry[tid] = (int8_t)e_prev;
     if (tid < R) { s_neg[tid] = 0; s_zmin[tid] = INT_MAX; }
     __syncthreads();
-    // binary carry lookahead: w_l = u_l + e_(l-1) generates g_l (carry out) or propagates p_l
-    // (w_l = 2^64 - 1); carry into l + 1 = g_l | (p_l & carry into l).  (G, P) packed as bit 0 / 1.
-    int gp = 2;  // identity: G = 0, P = 1
-    int gbits = 0, pbits = 0;
-    int ein = k > 0 ? (int)s_ecarry[tid - R] : 0;
-#pragma unroll
-    for (int c = 0; c < CH; ++c) {
-        const uint64_t uv = u[c] + (uint64_t)ein;
-        const int g = uv < (uint64_t)ein ? 1 : 0;
-        const int pr = uv == ~0ull ? 1 : 0;
-        u[c] = uv;
-        gbits |= g << c;
-        pbits |= pr << c;
-        gp = (g | (pr & gp)) | ((pr & (gp >> 1)) << 1);
-        ein = e[c];
+    {  // limb 0 with the previous chunk's local carry; chunk (G, P) = (limbs 1..) o (limb 0)
+        int g0 = 0;
+        add64_count(v0l, v0h, g0, k > 0 ? (uint32_t)s_ecarry[tid - R] : 0u, 0u);
+        const uint32_t p0 = (v0l & v0h) == 0xffffffffu;
+        u[0] = (uint64_t)v0h << 32 | v0l;
+        gbits |= (uint32_t)g0;
+        pbits |= p0;
+        Gt = Gt | (Pt & (uint32_t)g0);
+        Pt &= p0;
     }
+    const int gp = (int)(Gt | (Pt << 1));  // (G, P) packed as bit 0 / 1
     // segmented scan over the chunks of each row (lanes r, r + R, ...): compose(later, earlier)
     auto gp_compose = [](int later, int earlier) {
         return ((later | ((later >> 1) & earlier)) & 1) | ((later & earlier) & 2);
@@ -732,16 +751,20 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     const int prev = __shfl_up_sync(0xffffffffu, incl, R);
     int carry = s_wcarry[warp * R + r];
     if (lane_r > 0) carry = (prev & 1) | ((prev >> 1) & carry);
-    int zloc = INT_MAX;
 #pragma unroll
     for (int c = 0; c < CH; ++c) {  // final limbs (mod 2^(64 Ly))
-        const uint64_t v = u[c] + (uint64_t)carry;
+        u[c] += (uint64_t)carry;
         carry = ((gbits >> c) & 1) | ((pbits >> c) & carry);
-        u[c] = v;
-        if (l0 + c < Ly && v && zloc == INT_MAX) zloc = l0 + c;
-        if (l0 + c == Ly - 1) s_neg[r] = (int)(v >> 63);
     }
-    if (zloc != INT_MAX) atomicMin(&s_zmin[r], zloc);
+    int zloc = INT_MAX;
+#pragma unroll
+    for (int c = CH - 1; c >= 0; --c) zloc = u[c] ? l0 + c : zloc;
+    if (zloc < Ly) atomicMin(&s_zmin[r], zloc);
+    if (l0 <= Ly - 1 && Ly - 1 < l0 + CH) {  // the row's top limb gives the sign
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+            if (l0 + c == Ly - 1) s_neg[r] = (int)(u[c] >> 63);
+    }
     __syncthreads();  // also: every CRT word has been read, the residue area is free
 #else
     // (c) all R rows at once: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R),
@@ -856,17 +879,15 @@ __global__ void __launch_bounds__(kK3Block, HK_K3_MINB) k3_finish(Params prm) {
     __syncthreads();  // also: every CRT word has been read, the residue area is free
 #endif
     uint64_t *ybuf = reinterpret_cast<uint64_t *>(sm);  // [R][Ly]
-    {
+    {  // two's complement -> magnitude: -Y = ~Y + 1, the + 1 rippling through the zero limbs
+       // below the lowest nonzero one (zmin): limb l -> (l <= zmin) + ~v
         const bool neg = s_neg[r] != 0;
         const int zmin = s_zmin[r];
+        const uint64_t m = neg ? ~0ull : 0ull;
+        uint64_t *yb = ybuf + r * Ly + l0;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-            const int l = l0 + c;
-            if (l < Ly) {
-                uint64_t v = u[c];
-                if (neg) v = l < zmin ? 0ull : (l == zmin ? (0ull - v) : ~v);
-                ybuf[r * Ly + l] = v;
-            }
+            if (l0 + c < Ly) yb[c] = (u[c] ^ m) + (uint64_t)(neg && l0 + c <= zmin);
         }
     }
     __syncthreads();
@@ -1086,7 +1107,7 @@ static int launch_k3(const Params &prm, cudaStream_t st, int64_t nrows) {
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
     const unsigned grid = (unsigned)((nrows + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
-    k3_finish<LOGN2, CH><<<grid, kK3Block, smem, st>>>(prm);
+    k3_finish<LOGN2, CH><<<grid, k3_threads<LOGN2>(), smem, st>>>(prm);
     return check_launch();
 }
 
@@ -1109,7 +1130,7 @@ static int k3_dispatch(const Params &prm, cudaStream_t st, int64_t nrows, int ch
 }
 template <int LOGN2>
 static int launch_k3_ch(const Params &prm, cudaStream_t st, int64_t nrows) {
-    constexpr int TR = kK3Block / k3_rows<LOGN2>();  // threads per row
+    constexpr int TR = k3_threads<LOGN2>() / k3_rows<LOGN2>();  // threads per row
     const int ch = (prm.Ly + TR - 1) / TR;
     if (ch < k3_ch_lo<LOGN2>()) return HK_EUNSUPPORTED;
     return k3_dispatch<LOGN2, k3_ch_lo<LOGN2>()>(prm, st, nrows, ch);

@@ -54,7 +54,7 @@ MICRO_GS, MICRO_CT = 12.07, 11.22  # butterflies / clk / SM
 # Garner coefficient of the CRT loop and per output limb of the carry phase.
 S_BFLY, S_PW, S_RES = 8, 6, 15
 S_CRT_SURVEY, S_CARRY_SURVEY = 110, 25
-C_CRT, C_CARRY = 110, 25
+C_CRT, C_CARRY = 112, 75  # profiles/r02/k3_sass_counts.json (k3_finish<10,13>)
 
 
 def survey_model(plan, m=None):
@@ -710,6 +710,8 @@ def main():
                                                   ("k3_finish", "K3", stage_ms[2]))}
         roof["kernels"]["k3_finish"]["frac_survey_constants"] = (
             sm_cnt["K3_survey_constants"] / (peak_tinstr * 1e12) / (stage_ms[2] * 1e-3))
+        t_alu_s = (sm_cnt["total"] - sm_cnt["K3"] + sm_cnt["K3_survey_constants"]) / (peak_tinstr * 1e12)
+        roof["step"]["step_frac_survey_constants"] = max(t_alu_s, t_hbm) / (ms_step * 1e-3)
         ach_bfly = cnt["k2_bfly_eq"] / (k2_ms * 1e-3) / 1e12
         roof["pipe_model"] = {
             "what": "secondary: K2 in GS-butterfly equivalents against the FMA-pipe limit (IMAD.HI 4 clk, "

@@ -65,11 +65,12 @@ __device__ __forceinline__ uint64_t smem_desc(const void *p) {
 constexpr uint32_t kIdesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(MMA_N >> 3) << 17) |
                             ((uint32_t)(NG >> 4) << 24);
 
+constexpr int TPAD = NK + 4;  // tile row stride (words): 144 B, an odd number of 16-byte units
 struct TcSmem {
-    uint32_t tile[NG][NK];                 // 16 KB: current residues
+    uint32_t tile[NG][TPAD];               // 18 KB: current residues
     alignas(1024) uint8_t a[NG * KB];      // 16 KB: A operand (group bytes)
     alignas(1024) uint8_t b[MMA_N * KB];   // 16 KB: B operand (constant F byte planes)
-    uint32_t tw[NG][NK], twq[NG][NK];      // 32 KB: twiddles + Shoup quotients
+    uint32_t tw[NK][NG], twq[NK][NG];      // 32 KB: twiddles + Shoup quotients, [k][group]
     alignas(8) uint64_t mbar;
     uint32_t tmem_base;
 };
@@ -82,9 +83,9 @@ __global__ void __launch_bounds__(THREADS, 1) tc_stage(const uint32_t *x_in, uin
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t *xin = x_in + (size_t)blockIdx.x * NG * NK;
     for (int i = tid; i < NG * NK; i += THREADS) {
-        (&S.tile[0][0])[i] = xin[i];
-        (&S.tw[0][0])[i] = tw[(size_t)blockIdx.x * NG * NK + i];
-        (&S.twq[0][0])[i] = twq[(size_t)blockIdx.x * NG * NK + i];
+        S.tile[i / NK][i % NK] = xin[i];
+        S.tw[i % NK][i / NK] = tw[(size_t)blockIdx.x * NG * NK + i];
+        S.twq[i % NK][i / NK] = twq[(size_t)blockIdx.x * NG * NK + i];
     }
     for (int i = tid; i < MMA_N * KB / 16; i += THREADS)
         reinterpret_cast<uint4 *>(S.b)[i] = reinterpret_cast<const uint4 *>(bmat)[i];
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_stage(const uint32_t *x_in, uin
                 const uint32_t L = d[4 * t] + (d[4 * t + 1] << 8);      // < 2^23 + 2^31
                 const uint32_t H = d[4 * t + 2] + (d[4 * t + 3] << 8);  // weight 2^16
                 const uint32_t v = addm(red1(shoup(H, r16, r16q, P), P), red1(shoup(L, 1u, onq, P), P), P);
-                y4[t] = red1(shoup(v, S.tw[n][k], S.twq[n][k], P), P);
+                y4[t] = red1(shoup(v, S.tw[k][n], S.twq[k][n], P), P);
             }
             *reinterpret_cast<uint4 *>(&S.tile[n][4 * kq]) = make_uint4(y4[0], y4[1], y4[2], y4[3]);
         }
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_stage(const uint32_t *x_in, uin
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     }
     uint32_t *yo = y_out + (size_t)blockIdx.x * NG * NK;
-    for (int i = tid; i < NG * NK; i += THREADS) yo[i] = (&S.tile[0][0])[i];
+    for (int i = tid; i < NG * NK; i += THREADS) yo[i] = S.tile[i / NK][i % NK];
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(128));
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_stage(const uint32_t *x_in, uin
 struct AluSmem {
     uint32_t tile[NG][NK + 1];
     uint32_t w[NK], wq[NK];                // w^j, j < 16 (table entries h + j as in the NTT path)
-    uint32_t tw[NG][NK], twq[NG][NK];
+    uint32_t tw[NK][NG], twq[NK][NG];      // [k][group]: consecutive lanes, consecutive banks
 };
 __global__ void __launch_bounds__(THREADS, 1) alu_stage(const uint32_t *x_in, uint32_t *y_out, const uint32_t *wt,
                                                          const uint32_t *wtq, const uint32_t *tw, const uint32_t *twq,
@@ -202,8 +203,8 @@ __global__ void __launch_bounds__(THREADS, 1) alu_stage(const uint32_t *x_in, ui
     const int tid = threadIdx.x;
     for (int i = tid; i < NG * NK; i += THREADS) {
         S.tile[i / NK][i % NK] = x_in[(size_t)blockIdx.x * NG * NK + i];
-        (&S.tw[0][0])[i] = tw[(size_t)blockIdx.x * NG * NK + i];
-        (&S.twq[0][0])[i] = twq[(size_t)blockIdx.x * NG * NK + i];
+        S.tw[i % NK][i / NK] = tw[(size_t)blockIdx.x * NG * NK + i];
+        S.twq[i % NK][i / NK] = twq[(size_t)blockIdx.x * NG * NK + i];
     }
     if (tid < NK) { S.w[tid] = wt[tid]; S.wq[tid] = wtq[tid]; }
     __syncthreads();
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(THREADS, 1) alu_stage(const uint32_t *x_in, ui
             }
         }
 #pragma unroll
-        for (int k = 0; k < NK; ++k) S.tile[n][k] = red1(shoup(v[k], S.tw[n][k], S.twq[n][k], P), P);
+        for (int k = 0; k < NK; ++k) S.tile[n][k] = red1(shoup(v[k], S.tw[k][n], S.twq[k][n], P), P);
     }
     __syncthreads();
     for (int i = tid; i < NG * NK; i += THREADS) y_out[(size_t)blockIdx.x * NG * NK + i] = S.tile[i / NK][i % NK];

@@ -312,6 +312,47 @@ int32_t hk_karatsuba_matvec(int64_t n, int32_t P, int32_t cutoff,
                             uint64_t *y_mag, int8_t *y_sign,
                             void *ws, size_t ws_bytes, void *stream);
 
+/* ---- F3: the paper's decomposition approach with a double-precision FFT ----
+ * PAPER.md P:119-170 decomposes every multiprecision number into standard-precision pieces and
+ * computes the product with one standard FFT, leaving open "whether the loss of accuracy occurs in
+ * practice".  This variant makes it exact with a PROOF: mantissas are cut into balanced
+ * w-bit digits (|d| <= 2^(w-1)), the 2-D convolution (matrix index x digit) is a complex FP64 FFT
+ * of N1 x N2 points with round-to-nearest butterflies, and the planner picks the widest w for which
+ * Percival's bound (Math. Comp. 72 (2003), Thm 5.1, with k = log2(N1 N2) radix-2 stages, unit
+ * roundoff eps = 2^-53 and twiddle error beta = 2^-52) on |computed - exact| of every output
+ * coefficient, evaluated with |a|_2 |x|_2 <= sqrt(a_count n) Ls 2^(2w-2), is <= 0.49; each
+ * coefficient is then rounded to its exact integer and carried into y (same layout, canonical
+ * form and exactness as hk_hankel_matvec).  Slower than the NTT path; supported for N1 <= 4096 and
+ * N2 <= 8192 (else HK_EUNSUPPORTED).  Square problems only (m = n), all three kinds. */
+typedef struct {
+    int32_t kind;
+    int32_t P;
+    int64_t m, n, a_count;
+    int32_t L, Ly;
+    int32_t w;             /* balanced digit width                                             */
+    int32_t Ls;            /* digits per mantissa = ceil(P / w) + 1                            */
+    int32_t log_n1;        /* matrix-index FFT length 2^log_n1                                 */
+    int32_t log_n2;        /* digit FFT length 2^log_n2 >= 2 Ls - 1                            */
+    int32_t cyclic, fold;  /* as hk_plan_info                                                  */
+    double bound;          /* Percival bound on the coefficient error (<= 0.49 < 1/2)          */
+    double eps, beta;      /* unit roundoff and twiddle error the bound assumes                */
+    uint64_t ws_bytes;     /* workspace bytes for hk_fft_workspace_init / hk_fft_matvec        */
+} hk_fft_plan_info;
+
+/* The plan (pure host; HK_EUNSUPPORTED when no digit width meets the bound within the limits). */
+int32_t hk_fft_plan(int32_t kind, int64_t n, int32_t P, hk_fft_plan_info *out);
+/* Twiddle tables (host-computed in long double, uploaded), carry table, header; stream-ordered.
+ * ws: >= info.ws_bytes DEVICE bytes, 256-byte aligned; HK_ENOMEM when smaller. */
+int32_t hk_fft_workspace_init(int32_t kind, int64_t n, int32_t P, void *ws, size_t ws_bytes,
+                              void *stream);
+/* y = A x through the FP64 FFT path; arguments, layouts, validation and the data-status word
+ * (hk_workspace_status) as hk_hankel_matvec / hk_toeplitz_matvec / hk_circulant_matvec (kind). */
+int32_t hk_fft_matvec(int32_t kind, int64_t n, int32_t P,
+                      const uint64_t *a_mag, const int8_t *a_sign,
+                      const uint64_t *x_mag, const int8_t *x_sign,
+                      uint64_t *y_mag, int8_t *y_sign,
+                      void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,19 @@ class PlanInfo(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class FftPlanInfo(ctypes.Structure):
+    """hk_fft_plan_info (include/hk.h): the F3 FP64-FFT plan and its Percival bound."""
+    _fields_ = [("kind", ctypes.c_int32), ("P", ctypes.c_int32), ("m", ctypes.c_int64),
+                ("n", ctypes.c_int64), ("a_count", ctypes.c_int64), ("L", ctypes.c_int32),
+                ("Ly", ctypes.c_int32), ("w", ctypes.c_int32), ("Ls", ctypes.c_int32),
+                ("log_n1", ctypes.c_int32), ("log_n2", ctypes.c_int32), ("cyclic", ctypes.c_int32),
+                ("fold", ctypes.c_int32), ("bound", ctypes.c_double), ("eps", ctypes.c_double),
+                ("beta", ctypes.c_double), ("ws_bytes", ctypes.c_uint64)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class ShardInfo(ctypes.Structure):
     """hk_shard_info (include/hk.h): sigma-coset sharding layout."""
     _fields_ = [("G", ctypes.c_int32), ("gamma", ctypes.c_int32), ("block_cols", ctypes.c_int64),
@@ -99,6 +112,9 @@ def _load():
         "hk_hankel_shard_finish_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_prepared": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_fft_plan": (i32, [i32, i64, i32, ctypes.POINTER(FftPlanInfo)]),
+        "hk_fft_workspace_init": (i32, [i32, i64, i32, vp, sz, vp]),
+        "hk_fft_matvec": (i32, [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -114,7 +130,8 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_schoolbook_matvec", "hk_matvec_stages", "hk_karatsuba_workspace_size",
             "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared", "hk_shard_plan",
             "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish",
-            "hk_matvec_rounded", "hk_hankel_shard_forward_p2p", "hk_hankel_shard_finish_p2p")
+            "hk_matvec_rounded", "hk_hankel_shard_forward_p2p", "hk_hankel_shard_finish_p2p",
+            "hk_fft_plan", "hk_fft_workspace_init", "hk_fft_matvec")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -630,6 +647,57 @@ def karatsuba_matvec(a_mag, a_sign, x_mag, x_sign, P, cutoff: int = 8, out=None,
     # the current stream, so tell the allocator the work on `stream` still uses it
     if stream is not None:
         buf.record_stream(stream)
+    return out
+
+
+# ---- F3: the paper's decomposition approach with a double-precision FFT (exact by Percival's bound)
+def fft_plan(kind: int, n: int, P: int) -> dict:
+    """The FP64-FFT plan (digit width w, lengths, Percival bound); pure host call."""
+    info = FftPlanInfo()
+    _check(_lib.hk_fft_plan(int(kind), int(n), int(P), ctypes.byref(info)), "hk_fft_plan")
+    return info.as_dict()
+
+
+class FftWorkspace:
+    """Device workspace of the F3 path (twiddle tables, carry table, 2 x N1 x N2 complex doubles)."""
+
+    def __init__(self, kind, n, P, device=None, stream=None):
+        import torch
+        self.kind, self.n, self.P = int(kind), int(n), int(P)
+        self.info = fft_plan(kind, n, P)
+        self.nbytes = int(self.info["ws_bytes"])
+        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8,
+                               device=device or torch.device("cuda", torch.cuda.current_device()))
+        self.ptr = (self.buf.data_ptr() + 255) & ~255
+        _check(_lib.hk_fft_workspace_init(self.kind, self.n, self.P, self.ptr, self.nbytes,
+                                          _stream_ptr(stream)), "hk_fft_workspace_init")
+
+    status = Workspace.status
+
+
+def fft_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, out=None, ws=None, stream=None, check=True):
+    """y = A x exactly through the FP64 FFT path (hk_fft_matvec): same layouts as matvec()."""
+    import torch
+    n = int(x_mag.shape[0])
+    L, Ly = limbs(P), out_limbs(P)
+    na = n if kind == CIRCULANT else 2 * n - 1
+    args = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (n,), "x_sign")]
+    if out is None:
+        out = (torch.empty((n, Ly), dtype=a_mag.dtype, device=a_mag.device),
+               torch.empty((n,), dtype=torch.int8, device=a_mag.device))
+    args += [_dev_ptr(out[0], _mag_dtypes(), (n, Ly), "y_mag"),
+             _dev_ptr(out[1], (torch.int8,), (n,), "y_sign")]
+    if ws is None:
+        ws = FftWorkspace(kind, n, P, stream=stream)
+    if (ws.kind, ws.n, ws.P) != (int(kind), n, int(P)):
+        raise ValueError("FFT workspace was initialised for a different problem")
+    _check(_lib.hk_fft_matvec(int(kind), n, int(P), *args, ws.ptr, ws.nbytes, _stream_ptr(stream)),
+           "hk_fft_matvec")
+    if check:
+        _check(ws.status(stream), "hk_fft_matvec data status")
     return out
 
 

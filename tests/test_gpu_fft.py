@@ -1,0 +1,112 @@
+"""GPU parity of the F3 path (hk_fft_matvec: the paper's decomposition approach with an FP64 FFT,
+PAPER.md P:119-170, made exact by Percival's bound -- tests/test_fft_bound.py pins the planner):
+bit-exact against the oracle element by element, on every kind, ragged and edge sizes, the
+carry-stress recipe, the closed forms with max-magnitude entries (the norms the bound assumes), and
+the BASELINE configs the variant supports (C1; C2 and C5-circulant via the committed oracle
+digests)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import hkinputs as gen
+import oracle
+from oracle import bruteforce as bf
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+DIG = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "digests")
+
+
+@pytest.fixture(scope="module")
+def hk():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1402_5287_b200 as hk
+    return hk
+
+
+def run_fft(hk, kind, am, asg, xm, xsg, P):
+    ym, ys = hk.fft_matvec(kind, *hk.to_device(am, asg), *hk.to_device(xm, xsg), P)
+    torch.cuda.synchronize()
+    return hk.to_host(ym, ys)
+
+
+def assert_same(got, want, ctx=""):
+    gm, gs = got
+    wm, ws = want
+    bad = np.nonzero((gm != wm).any(axis=1) | (gs != ws))[0]
+    assert bad.size == 0, f"{ctx}: {bad.size} rows differ, first {bad[:8]}"
+
+
+def test_c1_all_kinds(hk):
+    for kind in (0, 1, 2):
+        am, asg, xm, xsg = gen.make_inputs(kind, 64, 3328, 0)
+        assert_same(run_fft(hk, kind, am, asg, xm, xsg, 3328), oracle.matvec(kind, 3328, am, asg, xm, xsg),
+                    f"C1 kind={kind}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 17, 100, 257])
+@pytest.mark.parametrize("P", [1, 64, 65, 1000, 5000])
+def test_edge_sizes(hk, n, P):
+    for kind in (0, 1, 2):
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=7 * n + P)
+        assert_same(run_fft(hk, kind, am, asg, xm, xsg, P), oracle.matvec(kind, P, am, asg, xm, xsg),
+                    f"kind={kind} n={n} P={P}")
+
+
+def test_carry_stress(hk):
+    for kind, n in ((1, 200), (2, 256), (2, 77)):
+        am, asg, xm, xsg = gen.make_inputs(kind, n, 4000, seed=4, recipe="carry_stress")
+        assert_same(run_fft(hk, kind, am, asg, xm, xsg, 4000), oracle.matvec(kind, 4000, am, asg, xm, xsg),
+                    f"carry-stress kind={kind} n={n}")
+
+
+def test_closed_forms_max_magnitude(hk):
+    """All entries +(2^P - 1): every digit of the balanced recoding is at its extreme, the largest
+    coefficients the bound covers; Y_i = n (2^P - 1)^2 (and the alternating-sign cancellation)."""
+    for n, P in ((7, 3328), (64, 16608), (300, 1000), (1000, 2000)):
+        Mx = (1 << P) - 1
+        for kind in (0, 1, 2):
+            am, asg = gen.max_magnitude(gen.a_count(kind, n), P)
+            xm, xsg = gen.max_magnitude(n, P)
+            assert_same(run_fft(hk, kind, am, asg, xm, xsg, P),
+                        bf.from_ints([n * Mx * Mx] * n, gen.n_out_limbs(P)), f"max n={n} P={P} kind={kind}")
+        am, asg = gen.max_magnitude(2 * n - 1, P)
+        xm, xsg = gen.max_magnitude(n, P, signs=[(-1) ** j for j in range(1, n + 1)])
+        assert_same(run_fft(hk, 0, am, asg, xm, xsg, P),
+                    bf.from_ints([0 if n % 2 == 0 else -Mx * Mx] * n, gen.n_out_limbs(P)), f"alternating n={n}")
+
+
+@pytest.mark.parametrize("name", ["C2", "C5C"])
+def test_config_digest(hk, name):
+    meta = json.load(open(os.path.join(DIG, f"{name}.json")))
+    c = gen.CONFIGS[name]
+    am, asg, xm, xsg = gen.config_inputs(name)
+    gm, gs = run_fft(hk, c["kind"], am, asg, xm, xsg, c["P"])
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(gm).tobytes())
+    h.update(np.ascontiguousarray(gs).tobytes())
+    assert h.hexdigest() == meta["y_sha256"], f"{name}: FFT-path y differs from the oracle digest"
+
+
+def test_rejects_bits_above_P(hk):
+    P = 300
+    am, asg, xm, xsg = gen.make_inputs(0, 20, P, seed=3)
+    am = am.copy()
+    am[2, -1] |= np.uint64(1) << np.uint64(63)
+    with pytest.raises(hk.HKError):
+        run_fft(hk, 0, am, asg, xm, xsg, P)
+
+
+def test_workspace_reuse(hk):
+    n, P = 150, 3000
+    ws = hk.FftWorkspace(0, n, P)
+    for seed in (1, 2):
+        am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=seed)
+        a, sa = hk.to_device(am, asg)
+        x, sx = hk.to_device(xm, xsg)
+        got = hk.to_host(*hk.fft_matvec(0, a, sa, x, sx, P, ws=ws))
+        assert_same(got, oracle.matvec(0, P, am, asg, xm, xsg), f"reuse seed={seed}")

@@ -560,6 +560,47 @@ def main():
                    "what": "hk_matvec_rounded: y = round_half_even(Y / 2^P), L+1 limbs (SURVEY 8(f) F4)"}
         del wsr, yr
 
+    # ---- F3 (secondary): the same matvec through the exact FP64 double-FFT path (hk_fft_matvec;
+    # the paper's decomposition approach, with Percival's bound)
+    fp64 = None
+    if rank == 0 and world == 1:
+        fpl = hk.fft_plan(kind, n, P)
+        fws = hk.FftWorkspace(kind, n, P)
+        yf = (torch.empty((n, plan["Ly"]), dtype=torch.int64, device=dev),
+              torch.empty((n,), dtype=torch.int8, device=dev))
+        hk.fft_matvec(kind, a, sa, x, sx, P, out=yf, ws=fws)
+        okf, whyf = verify_y(kind, am, asg, xm, xsg, yf[0], yf[1], 0, 1, None, dev)
+        if not okf:
+            raise SystemExit(f"bench: FP64-FFT y fails its fingerprints ({whyf})")
+        Kf = max(3, min(K, 20))
+        for _ in range(2):
+            hk.fft_matvec(kind, a, sa, x, sx, P, out=yf, ws=fws, check=False)
+        f0_, f1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0_.record(stream)
+        for _ in range(Kf):
+            hk.fft_matvec(kind, a, sa, x, sx, P, out=yf, ws=fws, check=False)
+        f1_.record(stream)
+        torch.cuda.synchronize()
+        if fws.status() != hk.HK_OK:
+            raise SystemExit("bench: FP64-FFT status not OK")
+        fms = f0_.elapsed_time(f1_) / Kf
+        N1f, N2f = 1 << fpl["log_n1"], 1 << fpl["log_n2"]
+        bfl = ((fpl["a_count"] + 2 * n) * (N2f // 2) * fpl["log_n2"] +
+               3 * N2f * (N1f // 2) * fpl["log_n1"])  # complex radix-2 butterflies
+        dp_ops = 10 * bfl  # 4 DMUL + 2 DADD (complex product) + 4 DADD per butterfly, no FMA
+        nsm_ = torch.cuda.get_device_properties(dev).multi_processor_count
+        smx_ = float(json.load(open(PEAKS_FILE)).get("sm_max_mhz", 1965.0)) if os.path.exists(PEAKS_FILE) else 1965.0
+        dp_peak = nsm_ * 56 * smx_ * 1e6  # FP64 lanes / clk / SM measured (profiles/r01/micro_fp64.log)
+        fp64 = {"value": 1000.0 / fms, "unit": UNIT, "ms_per_step": fms, "steps": Kf,
+                "plan": {k_: fpl[k_] for k_ in ("w", "Ls", "log_n1", "log_n2", "bound")},
+                "verified": "fingerprints of every row (mod 3 primes) before timing",
+                "fp64_ops": dp_ops, "fp64_peak_ops_s": dp_peak,
+                "fp64_frac": dp_ops / (fms * 1e-3) / dp_peak,
+                "what": "hk_fft_matvec: balanced w-bit digits, 2-D complex FP64 FFT convolution with a proven "
+                        "< 1/2 error (Percival), rint, carry (SURVEY 8(f) F3); ops = 10 per complex butterfly "
+                        "against 56 FP64 lanes/clk/SM"}
+        del fws, yf
+
     # ---- e2e through the host-buffer C-ABI call (N = 1 workload per rank)
     e2e = None
     if rank == 0 and not args.no_e2e and world == 1:
@@ -755,6 +796,7 @@ def main():
         "e2e": e2e,
         "warm_a": warm,
         "rounded": rounded,
+        "fp64_fft": fp64,
         "throughput": throughput,
         "gpu_launches": launches_per_step * K,
         "clocks": clocks,

@@ -322,7 +322,7 @@ int32_t hk_karatsuba_matvec(int64_t n, int32_t P, int32_t cutoff,
  * roundoff eps = 2^-53 and twiddle error beta = 2^-52) on |computed - exact| of every output
  * coefficient, evaluated with |a|_2 |x|_2 <= sqrt(a_count n) Ls 2^(2w-2), is <= 0.49; each
  * coefficient is then rounded to its exact integer and carried into y (same layout, canonical
- * form and exactness as hk_hankel_matvec).  Slower than the NTT path; supported for N1 <= 4096 and
+ * form and exactness as hk_hankel_matvec).  Slower than the NTT path; supported for N1 <= 32768 and
  * N2 <= 8192 (else HK_EUNSUPPORTED).  Square problems only (m = n), all three kinds. */
 typedef struct {
     int32_t kind;

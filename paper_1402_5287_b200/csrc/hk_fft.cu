@@ -21,8 +21,10 @@
 //            128-bit sum of the coefficients whose bit offset falls in it, then the binary carry
 //            lookahead of K3 v2 and -Cb sum_s 2^(w s) added limb by limb (table in the workspace).
 //
-// Scope of this variant: N1 <= 4096 (the column FFTs of a and x held in shared memory) and
-// N2 <= 8192 -- BASELINE configs C1, C2 and C5-circulant.  The NTT path stays the product headline.
+// Scope: N2 <= 8192, N1 <= 32768 -- every BASELINE config.  N1 <= 4096: a column pair of a and x
+// in shared memory per CTA (F2); N1 = 2^(12+g): the first g forward and last g inverse column stages
+// run from HBM (f2_top / f2_bottom) around 4096-point blocks in shared memory.  The NTT path stays
+// the product headline (this one moves complex doubles: ~20 GB of HBM traffic per C3 matvec).
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -39,7 +41,7 @@ namespace hk {
 namespace {
 
 constexpr uint64_t kFftMagic = 0x484b464654504c4eull;  // "HKFFTPLN"
-constexpr int kFftMaxLogN1 = 12, kFftMaxLogN2 = 13, kFftMinLog = 5;
+constexpr int kFftMaxLogN1 = 15, kFftMaxLogN2 = 13, kFftMinLog = 5;
 constexpr int kFftPad = 1024;  // -K table entries past Ly
 
 struct FftPlan {
@@ -202,15 +204,19 @@ __global__ void __launch_bounds__(kFftThreads) f1_rows(FftParams prm) {
 
 // F2: per pair of columns: forward column FFTs (N1) of a and x, pointwise product, inverse FFT;
 // the result replaces x's columns (all N1 rows)
-template <int LOGN1, int TC>
+// SPLIT (N1 > 2^LOGN1 = 4096): block blockIdx.y of 4096 consecutive rows after f2_top's first
+// stages; the block is then an independent 4096-point transform (its stages' twiddles are the
+// N1 table's first 4096 entries) and every row holds data (no zero masking)
+template <int LOGN1, int TC, bool SPLIT>
 __global__ void __launch_bounds__(kFftThreads) f2_cols(FftParams prm) {
     constexpr int N1 = 1 << LOGN1, RS = N1 + N1 / 8;
     extern __shared__ double2 cs[];  // [2 arrays][TC columns][RS]
     const int sig0 = blockIdx.x * TC, N2 = prm.N2;
-    const int64_t na = prm.a_count, nx = prm.n;
+    const int64_t na = SPLIT ? N1 : prm.a_count, nx = SPLIT ? N1 : prm.n;
+    const size_t row0 = SPLIT ? (size_t)blockIdx.y * N1 : 0;
     for (int e = threadIdx.x; e < N1 * TC; e += blockDim.x) {
         const int i = e / TC, c = e % TC;
-        const size_t g = (size_t)i * N2 + sig0 + c;
+        const size_t g = (row0 + i) * N2 + sig0 + c;
         cs[c * RS + cpad(i)] = i < na ? prm.A[g] : make_double2(0.0, 0.0);
         cs[(TC + c) * RS + cpad(i)] = i < nx ? prm.X[g] : make_double2(0.0, 0.0);
     }
@@ -225,7 +231,75 @@ __global__ void __launch_bounds__(kFftThreads) f2_cols(FftParams prm) {
     CDit<LOGN1, 0>::run(cs + TC * RS, TC, RS, prm.tw1);
     for (int e = threadIdx.x; e < N1 * TC; e += blockDim.x) {
         const int i = e / TC, c = e % TC;
-        prm.X[(size_t)i * N2 + sig0 + c] = cs[(TC + c) * RS + cpad(i)];
+        prm.X[(row0 + i) * N2 + sig0 + c] = cs[(TC + c) * RS + cpad(i)];
+    }
+}
+
+// N1 = 2^(12 + GAMMA) > 4096: the first GAMMA forward stages (half-sizes N1/2 .. 4096) of the a and
+// x columns from HBM, in place; thread item = (array, j0 < 4096, sigma), sigma fastest (coalesced)
+template <int GAMMA>
+__global__ void __launch_bounds__(256) f2_top(FftParams prm) {
+    constexpr int G = 1 << GAMMA, S = 4096;
+    const int N2 = prm.N2;
+    const int64_t items = (int64_t)2 * S * N2;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int sig = (int)(it % N2);
+        const int64_t rest = it / N2;
+        const int j0 = (int)(rest % S);
+        const bool isx = rest >= S;
+        double2 *arr = isx ? prm.X : prm.A;
+        const int64_t cnt = isx ? prm.n : prm.a_count;
+        double2 v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) {
+            const int64_t i = j0 + (int64_t)m * S;
+            v[m] = i < cnt ? arr[i * N2 + sig] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int l = GAMMA - 1; l >= 0; --l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                const int j = j0 + S * (m & (half - 1));
+                const double2 d = csub(v[m], v[m + half]);
+                v[m] = cadd(v[m], v[m + half]);
+                v[m + half] = cmul(d, __ldg(prm.tw1 + S * half + j));
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m) arr[(j0 + (int64_t)m * S) * N2 + sig] = v[m];
+    }
+}
+
+// ... and the last GAMMA inverse stages (half-sizes 4096 .. N1/2) of the product, in place
+template <int GAMMA>
+__global__ void __launch_bounds__(256) f2_bottom(FftParams prm) {
+    constexpr int G = 1 << GAMMA, S = 4096;
+    const int N2 = prm.N2;
+    const int64_t items = (int64_t)S * N2;
+    for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
+         it += (int64_t)gridDim.x * blockDim.x) {
+        const int sig = (int)(it % N2);
+        const int j0 = (int)(it / N2);
+        double2 v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) v[m] = prm.X[(j0 + (int64_t)m * S) * N2 + sig];
+#pragma unroll
+        for (int l = 0; l < GAMMA; ++l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                const int j = j0 + S * (m & (half - 1));
+                const double2 t = cmulc(v[m + half], __ldg(prm.tw1 + S * half + j));
+                v[m + half] = csub(v[m], t);
+                v[m] = cadd(v[m], t);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < G; ++m) prm.X[(j0 + (int64_t)m * S) * N2 + sig] = v[m];
     }
 }
 
@@ -518,12 +592,25 @@ int launch_rows_fft(const FftParams &prm, cudaStream_t st) {
 }
 template <int LOGN1>
 int launch_cols_fft(const FftParams &prm, cudaStream_t st) {
-    constexpr int TC = LOGN1 >= 12 ? 1 : 2;
-    const size_t sm = (size_t)2 * TC * ((1 << LOGN1) + (1 << LOGN1) / 8) * sizeof(double2);
-    if (cudaFuncSetAttribute(f2_cols<LOGN1, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+    constexpr bool SPLIT = LOGN1 > 12;
+    constexpr int LB = SPLIT ? 12 : LOGN1, TC = LB >= 12 ? 1 : 2;
+    const size_t sm = (size_t)2 * TC * ((1 << LB) + (1 << LB) / 8) * sizeof(double2);
+    if (cudaFuncSetAttribute(f2_cols<LB, TC, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
         return HK_ECUDA;
-    f2_cols<LOGN1, TC><<<(unsigned)(prm.N2 / TC), kFftThreads, sm, st>>>(prm);
-    return fft_check_launch();
+    constexpr int GAMMA = SPLIT ? LOGN1 - 12 : 0;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    if constexpr (SPLIT) {
+        f2_top<GAMMA><<<(unsigned)(nsm * 8), 256, 0, st>>>(prm);
+        if (const int rc = fft_check_launch()) return rc;
+    }
+    f2_cols<LB, TC, SPLIT><<<dim3((unsigned)(prm.N2 / TC), 1u << GAMMA), kFftThreads, sm, st>>>(prm);
+    if (const int rc = fft_check_launch()) return rc;
+    if constexpr (SPLIT) {
+        f2_bottom<GAMMA><<<(unsigned)(nsm * 8), 256, 0, st>>>(prm);
+        return fft_check_launch();
+    }
+    return HK_OK;
 }
 template <int LOGN2>
 int launch_finish_fft(const FftParams &prm, cudaStream_t st) {
@@ -554,7 +641,7 @@ int fft_run(const FftParams &prm, cudaStream_t st) {
     if (rc || (rc = fft_dbg("F1 rows", st))) return rc;
     switch (prm.log_n1) {
 #define HK_C(LG) case LG: rc = launch_cols_fft<LG>(prm, st); break;
-        HK_C(5) HK_C(6) HK_C(7) HK_C(8) HK_C(9) HK_C(10) HK_C(11) HK_C(12)
+        HK_C(5) HK_C(6) HK_C(7) HK_C(8) HK_C(9) HK_C(10) HK_C(11) HK_C(12) HK_C(13) HK_C(14) HK_C(15)
 #undef HK_C
         default: return HK_EUNSUPPORTED;
     }

@@ -89,6 +89,12 @@ constexpr int kK1Rows = HK_K1_ROWS;
 #ifndef HK_K1_L2PF
 #define HK_K1_L2PF 148  // tiles ahead whose limbs are bulk-prefetched into L2 (0: off)
 #endif
+// words of K1's transform area: the kK1Rows padded rows, or the tile's limbs if larger (16-byte
+// multiple, so the twiddle tables after it stay 16-byte aligned)
+__host__ __device__ inline int k1_transform_words(int rs, int L) {
+    const int t = kK1Rows * rs, l = kK1Rows * L * 2;
+    return ((t > l ? t : l) + 3) & ~3;
+}
 template <int LOGN2>
 constexpr int k1_threads() {
     return kK1Rows * ((1 << LOGN2) / 32 > 8 ? (1 << LOGN2) / 32 : 8);
@@ -136,8 +142,12 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
     const int64_t r0 = (int64_t)tile * kK1Rows;
     const int L = prm.L, w = prm.w, Ls = prm.Ls;
 
-    // ---- stage the tile's limbs (kK1Rows consecutive entries = one contiguous block) in smem
-    uint64_t *slimb = reinterpret_cast<uint64_t *>(sm + kK1Rows * RS);
+    // ---- stage the tile's limbs (kK1Rows consecutive entries = one contiguous block) in smem: in
+    // the transform area, dead until the first prime's top pass (the limbs fit: L <= N2 / 2 + 1
+    // for w >= 64); the two N2 twiddle tables live after it
+    uint64_t *slimb = reinterpret_cast<uint64_t *>(sm);
+    const int ta_words = k1_transform_words(RS, L);
+    uint2 *stw = reinterpret_cast<uint2 *>(sm + ta_words);
     {
         const int64_t nrows = count - r0 < kK1Rows ? count - r0 : kK1Rows;
         const int64_t bytes = nrows * L * 8;
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
     // N2 twiddle tables -> smem, double-buffered in the (now free) limb staging area: the table
     // of prime kp + 2 streams in by cp.async while prime kp is transformed
     auto fetch_tw = [&](int kp) {
-        uint4 *dst = reinterpret_cast<uint4 *>(slimb) + (kp & 1) * (N2 / 2);
+        uint4 *dst = reinterpret_cast<uint4 *>(stw) + (kp & 1) * (N2 / 2);
         const uint4 *src = reinterpret_cast<const uint4 *>(prm.tw + (size_t)kp * (prm.N2 + prm.N1));
         for (int i = tid; i < N2 / 2; i += T) cp_async16(dst + i, src + i);
         cp_async_commit();
@@ -233,7 +243,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         const uint32_t p = prm.pc[kp].p;
         const uint32_t *F = is_x ? prm.pc[kp].fx : prm.pc[kp].fa;
         const uint32_t *Fq = is_x ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
-        const uint2 *tw = reinterpret_cast<const uint2 *>(slimb) + (kp & 1) * N2;
+        const uint2 *tw = stw + (kp & 1) * N2;
         if (kp + 1 < kNumPrimes) cp_async_wait_group<1>();
         else cp_async_wait_group<0>();
         __syncthreads();
@@ -979,10 +989,8 @@ static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int nti
     if (ntiles <= 0) return HK_OK;
     Params prm = prm0;
     prm.tile0 = tile0;
-    const size_t limb_bytes = (size_t)kK1Rows * prm.L * sizeof(uint64_t);
-    const size_t tab_bytes = (size_t)2 * (1 << LOGN2) * sizeof(uint2);  // 2 tables, reuse the limb area
-    const size_t smem1 = (size_t)kK1Rows * k1_row_stride<LOGN2>() * sizeof(uint32_t) +
-                         (limb_bytes > tab_bytes ? limb_bytes : tab_bytes);
+    const size_t tab_bytes = (size_t)2 * (1 << LOGN2) * sizeof(uint2);  // 2 twiddle tables
+    const size_t smem1 = (size_t)k1_transform_words(k1_row_stride<LOGN2>(), prm.L) * sizeof(uint32_t) + tab_bytes;
     if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2, GAMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess)
         return HK_ECUDA;

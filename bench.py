@@ -470,6 +470,29 @@ def main():
                                  "(CUDA streams, each with its own prepared copy of a's transform); "
                                  "CUDA events on the calling stream, which waits for every lane"}
         del A, outs
+        # F1 kernel-level batch: one prepared copy of a's transform, 4 vectors per launch of each kernel
+        KB_ = 4
+        A = hk.PreparedMatrix(kind, a, sa, P, n, batch=KB_)
+        xb_m = x.unsqueeze(0).expand(KB_, -1, -1).contiguous()
+        xb_s = sx.unsqueeze(0).expand(KB_, -1).contiguous()
+        yb4 = (torch.empty((KB_, n, plan["Ly"]), dtype=torch.int64, device=dev),
+               torch.empty((KB_, n), dtype=torch.int8, device=dev))
+        for _ in range(W):
+            A.matvec_stacked(xb_m, xb_s, out=yb4, check=False)
+        torch.cuda.synchronize()
+        w0.record(stream)
+        for _ in range(K):
+            A.matvec_stacked(xb_m, xb_s, out=yb4, check=False)
+        w1.record(stream)
+        torch.cuda.synchronize()
+        if A.ws.status() != hk.HK_OK:
+            raise SystemExit("bench: kernel-batched prepared-matvec status not OK")
+        kbms = w0.elapsed_time(w1) / (K * KB_)
+        warm["kernel_batch"] = {"value": 1000.0 / kbms, "unit": UNIT, "ms_per_matvec": kbms, "vectors_per_launch": KB_,
+                                "what": "PreparedMatrix(batch=4).matvec_stacked -> hk_matvec_prepared_batch: one launch "
+                                        "of K1 / K2 / K3 for 4 vectors, one prepared copy of a's transform (each A^ "
+                                        "column read from HBM once per batch)"}
+        del A, xb_m, xb_s, yb4
 
     # ---- throughput mode: a stream of >= 16 independent matvecs with several
     # in flight; at N = 1 three Problems (own workspaces and y) on three streams, at N > 1 the

@@ -312,6 +312,26 @@ int32_t hk_karatsuba_matvec(int64_t n, int32_t P, int32_t cutoff,
                             uint64_t *y_mag, int8_t *y_sign,
                             void *ws, size_t ws_bytes, void *stream);
 
+/* ---- F1 kernel-level batch: nvec vectors against one prepared matrix, one launch per stage ----
+ * The paper's Lanczos use multiplies one matrix by many vectors.  A batch workspace is a
+ * HK_WS_PREPARED workspace followed by nvec per-vector transform regions (hk_batch_workspace_size,
+ * pure host; hk_batch_workspace_init, stream-ordered; the same 256-byte alignment rules).  After
+ * hk_prepare_a on it, hk_matvec_prepared_batch computes y_v = A x_v for v < nvec with ONE launch of
+ * each of K1 (x slicing), K2 (every A^ column read from HBM once for all vectors) and K3:
+ *   x_mag: uint64[nvec][n][L] (each vector 16-byte aligned: n L even or nvec = 1), x_sign: int8[nvec][n]
+ *   y_mag: uint64[nvec][m][Ly],  y_sign: int8[nvec][m]    (DEVICE; layouts as hk_matvec_prepared)
+ * ws_bytes must be the size the workspace was initialised with (its vector capacity is derived
+ * from it; HK_ENOMEM when nvec exceeds it).  The data-status word covers the whole batch (any
+ * rejected x -> HK_ERANGE for the call). */
+int32_t hk_batch_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
+                                size_t *bytes);
+int32_t hk_batch_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
+                                void *ws, size_t ws_bytes, void *stream);
+int32_t hk_matvec_prepared_batch(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
+                                 const uint64_t *x_mag, const int8_t *x_sign,
+                                 uint64_t *y_mag, int8_t *y_sign,
+                                 void *ws, size_t ws_bytes, void *stream);
+
 /* ---- F3: the paper's decomposition approach with a double-precision FFT ----
  * PAPER.md P:119-170 decomposes every multiprecision number into standard-precision pieces and
  * computes the product with one standard FFT, leaving open "whether the loss of accuracy occurs in

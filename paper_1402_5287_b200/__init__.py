@@ -112,6 +112,9 @@ def _load():
         "hk_hankel_shard_finish_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_prepared": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_batch_workspace_size": (i32, [i32, i64, i64, i32, i32, ctypes.POINTER(sz)]),
+        "hk_batch_workspace_init": (i32, [i32, i64, i64, i32, i32, vp, sz, vp]),
+        "hk_matvec_prepared_batch": (i32, [i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_fft_plan": (i32, [i32, i64, i32, ctypes.POINTER(FftPlanInfo)]),
         "hk_fft_workspace_init": (i32, [i32, i64, i32, vp, sz, vp]),
         "hk_fft_matvec": (i32, [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
@@ -131,7 +134,8 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_karatsuba_matvec", "hk_prepare_a", "hk_matvec_prepared", "hk_shard_plan",
             "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish",
             "hk_matvec_rounded", "hk_hankel_shard_forward_p2p", "hk_hankel_shard_finish_p2p",
-            "hk_fft_plan", "hk_fft_workspace_init", "hk_fft_matvec")
+            "hk_fft_plan", "hk_fft_workspace_init", "hk_fft_matvec", "hk_batch_workspace_size",
+            "hk_batch_workspace_init", "hk_matvec_prepared_batch")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -496,23 +500,54 @@ class Problem:
         return self.y_mag, self.y_sign
 
 
+class BatchWorkspace:
+    """A prepared workspace plus `nvec` per-vector transform regions (hk_batch_workspace_size/init)."""
+
+    def __init__(self, kind, n, P, m=None, nvec=2, device=None, stream=None):
+        import torch
+        self.kind, self.n, self.P = int(kind), int(n), int(P)
+        self.m = self.n if m is None else int(m)
+        self.nvec = int(nvec)
+        out = ctypes.c_size_t()
+        _check(_lib.hk_batch_workspace_size(self.kind, self.m, self.n, self.P, self.nvec, ctypes.byref(out)),
+               "hk_batch_workspace_size")
+        self.nbytes = int(out.value)
+        self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8,
+                               device=device or torch.device("cuda", torch.cuda.current_device()))
+        self.ptr = (self.buf.data_ptr() + 255) & ~255
+        _check(_lib.hk_batch_workspace_init(self.kind, self.m, self.n, self.P, self.nvec, self.ptr,
+                                            self.nbytes, _stream_ptr(stream)), "hk_batch_workspace_init")
+
+    status = Workspace.status
+    status_word = Workspace.status_word
+
+
 class PreparedMatrix:
     """F1 (fixed-A repeated products, the paper's Lanczos use P:32-36): the 2-D transform of a is
     computed once (hk_prepare_a) and reused by every matvec(x) (hk_matvec_prepared)."""
 
-    def __init__(self, kind, a_mag, a_sign, P, n, m=None, stream=None, check=True, lanes=1):
+    def __init__(self, kind, a_mag, a_sign, P, n, m=None, stream=None, check=True, lanes=1, batch=1):
         """lanes > 1: multi-vector batching for matvec_batch() -- that many CUDA streams, each with
         its own prepared workspace (a's transform computed once per lane), so several vectors'
-        products are in flight at once and fill each other's partial last waves."""
+        products are in flight at once and fill each other's partial last waves.
+        batch > 1: kernel-level batching instead -- ONE prepared copy of a's transform and room for
+        `batch` vectors; matvec_stacked() / matvec_batch() run up to `batch` vectors per launch of
+        each kernel (hk_matvec_prepared_batch; every A^ column read from HBM once per batch)."""
         import torch
         self.kind, self.P, self.n = int(kind), int(P), int(n)
         self.m = self.n if m is None else int(m)
+        self.batch = max(1, int(batch))
+        if self.batch > 1 and int(lanes) > 1:
+            raise ValueError("choose lanes (stream-level) or batch (kernel-level) batching, not both")
         L = limbs(P)
         na = (self.n if kind == CIRCULANT else self.m + self.n - 1)
         self.a = (a_mag, a_sign)
         pa = _dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag")
         ps = _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign")
-        self.ws = Workspace(kind, self.n, P, m=self.m, flags=WS_PREPARED, stream=stream)
+        if self.batch > 1:
+            self.ws = BatchWorkspace(kind, self.n, P, m=self.m, nvec=self.batch, stream=stream)
+        else:
+            self.ws = Workspace(kind, self.n, P, m=self.m, flags=WS_PREPARED, stream=stream)
         _check(_lib.hk_prepare_a(self.kind, self.m, self.n, self.P, pa, ps, self.ws.ptr,
                                  self.ws.nbytes, _stream_ptr(stream)), "hk_prepare_a")
         if check:
@@ -551,12 +586,53 @@ class PreparedMatrix:
             _check(self.ws.status(stream), "hk_matvec_prepared data status")
         return out
 
+    def matvec_stacked(self, x_mag, x_sign, out=None, stream=None, check=True):
+        """Kernel-level batch: x_mag [v, n, L], x_sign [v, n] with v <= batch -> (y_mag [v, m, Ly],
+        y_sign [v, m]) through hk_matvec_prepared_batch (one launch per kernel for all v)."""
+        import torch
+        if self.batch < 2:
+            raise ValueError("matvec_stacked needs PreparedMatrix(..., batch=k), k > 1")
+        L, Ly = limbs(self.P), out_limbs(self.P)
+        v = int(x_mag.shape[0])
+        if not 1 <= v <= self.batch:
+            raise ValueError(f"at most {self.batch} vectors per call")
+        px = _dev_ptr(x_mag, _mag_dtypes(), (v, self.n, L), "x_mag")
+        pxs = _dev_ptr(x_sign, (torch.int8,), (v, self.n), "x_sign")
+        if out is None:
+            out = (torch.empty((v, self.m, Ly), dtype=x_mag.dtype, device=x_mag.device),
+                   torch.empty((v, self.m), dtype=torch.int8, device=x_mag.device))
+        py = _dev_ptr(out[0], _mag_dtypes(), (v, self.m, Ly), "y_mag")
+        pys = _dev_ptr(out[1], (torch.int8,), (v, self.m), "y_sign")
+        _check(_lib.hk_matvec_prepared_batch(self.kind, self.m, self.n, self.P, v, px, pxs, py, pys,
+                                             self.ws.ptr, self.ws.nbytes, _stream_ptr(stream)),
+               "hk_matvec_prepared_batch")
+        if check:
+            _check(self.ws.status(stream), "hk_matvec_prepared_batch data status")
+        return out
+
     def matvec_batch(self, xs, outs=None, stream=None, check=True):
         """y_v = A x_v for a list of (x_mag, x_sign) pairs, distributed round-robin over the lanes
-        (see __init__); ordered after and before the calling stream.  Returns the list of outputs."""
+        (see __init__), or stacked into kernel-level batches of `batch` vectors; ordered after and
+        before the calling stream.  Returns the list of outputs."""
         import torch
         L, Ly = limbs(self.P), out_limbs(self.P)
         cur = torch.cuda.current_stream() if stream is None else stream
+        if self.batch > 1:
+            res = []
+            # stacked vectors must each start 16-byte aligned: n L even (else one vector per launch)
+            step = self.batch if (self.n * L) % 2 == 0 else 1
+            for g0 in range(0, len(xs), step):
+                grp = xs[g0:g0 + step]
+                ym, ys = self.matvec_stacked(torch.stack([xm for xm, _ in grp]),
+                                             torch.stack([xsg for _, xsg in grp]), stream=cur, check=check)
+                for v in range(len(grp)):
+                    if outs is not None:
+                        outs[g0 + v][0].copy_(ym[v])
+                        outs[g0 + v][1].copy_(ys[v])
+                        res.append(outs[g0 + v])
+                    else:
+                        res.append((ym[v], ys[v]))
+            return res
         if self.lanes == 1:
             return [self.matvec(xm, xsg, out=None if outs is None else outs[v], stream=cur, check=check)
                     for v, (xm, xsg) in enumerate(xs)]

@@ -190,6 +190,8 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     // K2 is split)
     if (!pl->split_k2) pl->off_AT = pl->off_end;
     pl->off_end_prepared = pl->split_k2 ? pl->off_end : align256(pl->off_AT + at_bytes);
+    pl->xhat_bytes = align256((size_t)kNumPrimes * N2loc * pl->ldX * 4);
+    pl->yhat_bytes = align256((size_t)kNumPrimes * N2 * pl->ldY * 4);
     in.ws_bytes = pl->off_end;
     in.ws_bytes_staging = pl->off_end_staging;
     in.ws_bytes_prepared = pl->off_end_prepared;
@@ -220,6 +222,7 @@ void fill_params(const Plan &pl, void *ws, Params *prm) {
     prm->reverse_out = pl.reverse_out; prm->x_reversed = pl.x_reversed;
     prm->out_off = pl.out_off;
     prm->ldA = pl.ldA; prm->ldX = pl.ldX; prm->ldY = pl.ldY;
+    prm->nvec = 1;
     prm->n2loc = prm->N2 / pl.G;
     prm->log_n2loc = in.log_n2 - pl.gamma;
     prm->shard_gamma = pl.gamma;
@@ -500,6 +503,76 @@ int32_t hk_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_
     Params prm;
     fill_params(pl, ws, &prm);
     return init_workspace(pl, prm, ws, stream);
+}
+
+// ---- F1 kernel-level batch: a prepared workspace followed by nvec X^ regions and nvec Y^ regions
+int32_t hk_batch_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
+                                size_t *bytes) {
+    if (!bytes || nvec < 1) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
+    if (rc) return rc;
+    *bytes = pl.info.ws_bytes_prepared + (size_t)nvec * (pl.xhat_bytes + pl.yhat_bytes);
+    return HK_OK;
+}
+
+int32_t hk_batch_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
+                                void *ws, size_t ws_bytes, void *stream) {
+    if (!ws || ((uintptr_t)ws & 255) != 0 || nvec < 1) return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
+    if (rc) return rc;
+    const size_t need = pl.info.ws_bytes_prepared + (size_t)nvec * (pl.xhat_bytes + pl.yhat_bytes);
+    if (ws_bytes < need) return HK_ENOMEM;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    if ((rc = init_workspace(pl, prm, ws, stream))) return rc;
+    // the vectors' X^ columns are zero-padded past n rows (K2's top pass reads ldX rows)
+    if (cudaMemsetAsync((char *)ws + pl.info.ws_bytes_prepared, 0, (size_t)nvec * pl.xhat_bytes,
+                        (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    return HK_OK;
+}
+
+int32_t hk_matvec_prepared_batch(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
+                                 const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
+                                 int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    if (!x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0 ||
+        ((uintptr_t)x_mag & 15) != 0 || nvec < 1 || nvec > 65535)
+        return HK_EINVAL;
+    Plan pl;
+    int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
+    if (rc) return rc;
+    // capacity of the workspace (its X^ regions come first, then its Y^ regions): from ws_bytes,
+    // which must be the size the workspace was initialised with
+    if (ws_bytes < pl.info.ws_bytes_prepared) return HK_ENOMEM;
+    const size_t cap = (ws_bytes - pl.info.ws_bytes_prepared) / (pl.xhat_bytes + pl.yhat_bytes);
+    if (cap < (size_t)nvec) return HK_ENOMEM;
+    const size_t need = pl.info.ws_bytes_prepared + cap * (pl.xhat_bytes + pl.yhat_bytes);
+    const size_t Ly = pl.info.Ly, L = pl.info.L, V = (size_t)nvec;
+    if (((n * L * 8) & 15) != 0 && nvec > 1) return HK_EINVAL;  // every vector 16-byte aligned
+    if (overlaps(y_mag, V * m * Ly * 8, x_mag, V * n * L * 8) || overlaps(y_sign, V * m, x_sign, V * n) ||
+        overlaps(y_mag, V * m * Ly * 8, ws, need) || overlaps(y_sign, V * m, ws, need))
+        return HK_EINVAL;
+    Params prm;
+    fill_params(pl, ws, &prm);
+    prm.x_mag = x_mag; prm.x_sign = x_sign; prm.y_mag = y_mag; prm.y_sign = y_sign;
+    prm.AT = (uint32_t *)((char *)ws + pl.off_AT);
+    prm.Xhat = (uint32_t *)((char *)ws + pl.info.ws_bytes_prepared);
+    prm.Yhat = (uint32_t *)((char *)ws + pl.info.ws_bytes_prepared + cap * pl.xhat_bytes);
+    prm.nvec = nvec;
+    prm.x_vstride = n;
+    prm.y_vstride = m;
+    prm.need_a_ready = 1;
+    if (pl.xhat_bytes != (size_t)kNumPrimes * prm.n2loc * prm.ldX * 4 ||
+        pl.yhat_bytes != (size_t)kNumPrimes * prm.N2 * prm.ldY * 4)
+        return HK_EUNSUPPORTED;  // vector regions must continue the column index (256-byte multiples)
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    const int ga = k1_tiles_a(prm);
+    if ((rc = launch_k1_range(prm, stream, ga, k1_tiles_x(prm)))) return rc;
+    if ((rc = launch_k2_mode(prm, stream, 2))) return rc;
+    return launch_k3_range(prm, stream, 0, m);
 }
 
 int32_t hk_workspace_status(void *ws, void *stream, int32_t *data_status) {

@@ -104,6 +104,11 @@ struct Params {
     GarnerConsts gc;
     Garner2Consts g2;
     const uint64_t *negK;        // Ly limbs of -K mod 2^(64 Ly) (K3 v2), in the workspace
+    // F1 kernel-level batch (hk_matvec_prepared_batch): nvec vectors per launch; vector v's x / y
+    // are x_vstride / y_vstride entries after vector v - 1's, its X^ / Y^ columns continue the
+    // column index (X^ column c of vector v = column v * ncols + c, likewise Y^); 1 otherwise
+    int32_t nvec;
+    int64_t x_vstride, y_vstride;
     const uint32_t *qmap;        // K3 v2: entry qq + 3 (qq = -3 .. Ly - 1) = (smem word offset of
                                  // the coefficient at limb qq, or of the zero slot) << 6 | shift
 };
@@ -118,6 +123,7 @@ struct Plan {
     size_t off_tw, off_negK, off_qmap, off_A, off_X, off_Y, off_stage, off_end, off_end_staging;
     size_t st_amag, st_asign, st_xmag, st_xsign, st_ymag, st_ysign;
     size_t off_AT, off_end_prepared;
+    size_t xhat_bytes, yhat_bytes;   // one vector's X^ / Y^ region (batch workspaces append nvec of each)
     int32_t split_k2;            // N1 >= 2^kSplitLogN1: AT inside the base layout, K2 in two launches
 };
 

@@ -359,22 +359,25 @@ HK_DEV void k2_prepare_body(const Params &prm, uint32_t *sm, const uint2 *twf, i
 
 // F1 prepared matvec: X^ forward, pointwise with the stored A^ transform, inverse.
 template <class TW, int LOGN1, bool SHARD = false>
-HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
+HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma,
+                             int vb = 0) {
     using PL = ColPlan<LOGN1>;
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
     const int tid = threadIdx.x;
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
-    const size_t cidx = (size_t)kp * prm.n2loc + sigma;
+    const size_t cidx = (size_t)kp * prm.n2loc + sigma;         // A^ (AT) column
+    const size_t ncols = (size_t)kNumPrimes * prm.n2loc;
+    const size_t cxy = (size_t)vb * ncols + cidx;                // X^ / Y^ column of batch vector vb
     const int nx = (int)prm.n;
     if (HK_K2_L2PF && tid == 0) {  // the stored A^ transform of this column and the next wave's X^
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(prm.AT + cidx * N1),
                      "r"((unsigned)(N1 * 4)) : "memory");
-        const size_t nxt = cidx + HK_K2_L2PF_NEXT;
-        if (HK_K2_L2PF_NEXT && nxt < (size_t)kNumPrimes * prm.n2loc)
+        const size_t nxt = cxy + HK_K2_L2PF_NEXT;
+        if (HK_K2_L2PF_NEXT && nxt < ncols * (size_t)prm.nvec)
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(prm.Xhat + nxt * prm.ldX),
                          "r"((unsigned)(prm.ldX * 4)) : "memory");
     }
-    k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
+    k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cxy * prm.ldX, nx <= N1 / 2, sm, twf, p);
     K2DifMiddle<TW, LOGN1, 1>::run(sm, twf, p);
     const uint32_t *at = prm.AT + cidx * N1;
 #pragma unroll
@@ -393,7 +396,7 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
         for (int m = 0; m < GL; ++m) sm[pad(g * GL) + m] = v[m];
     }
     __syncthreads();
-    k2_inverse_tail<TW, LOGN1, SHARD>(prm, sm, twf, p, cidx);
+    k2_inverse_tail<TW, LOGN1, SHARD>(prm, sm, twf, p, SHARD ? cidx : cxy);
 }
 
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
@@ -403,14 +406,17 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
 template <int LOGN1, class TW = TwGlobal, int MODE = 0>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
-    const int col = blockIdx.x;
+    // prepared batch (MODE 2, nvec vectors): consecutive CTAs take the same A^ column for the nvec
+    // vectors, so the stored AT column is read from HBM once and from L2 after that
+    const int col = MODE == 2 ? (int)(blockIdx.x / (unsigned)prm.nvec) : (int)blockIdx.x;
+    const int vb = MODE == 2 ? (int)(blockIdx.x % (unsigned)prm.nvec) : 0;
     const int kp = col >> prm.log_n2loc;  // columns (prime, sigma) held here: n2loc per prime
     const int sigma = col & (prm.n2loc - 1);
     const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1) + prm.N2;
     if constexpr (MODE == 0) k2_column_body<TW, LOGN1, false>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 3) k2_column_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 1) k2_prepare_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
-    else if constexpr (MODE == 2) k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
+    else if constexpr (MODE == 2) k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, sigma, vb);
     else k2_prepared_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);
 }
 

@@ -133,10 +133,11 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         return;
     }
     const int tile = is_x ? bt - tiles_a : bt;
-    const uint64_t *mag = is_x ? prm.x_mag : prm.a_mag;
-    const int8_t *sgn = is_x ? prm.x_sign : prm.a_sign;
+    const int64_t vb = (int64_t)blockIdx.y;  // batch vector (x tiles only; 0 otherwise)
+    const uint64_t *mag = is_x ? prm.x_mag + vb * prm.x_vstride * prm.L : prm.a_mag;
+    const int8_t *sgn = is_x ? prm.x_sign + vb * prm.x_vstride : prm.a_sign;
     const int64_t count = is_x ? prm.n : prm.a_count;
-    uint32_t *out = is_x ? prm.Xhat : prm.Ahat;
+    uint32_t *out = is_x ? prm.Xhat + vb * (int64_t)kNumPrimes * prm.n2loc * prm.ldX : prm.Ahat;
     const int64_t ld = is_x ? prm.ldX : prm.ldA;
     const bool rev = is_x && prm.x_reversed;
     const int64_t r0 = (int64_t)tile * kK1Rows;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
             const int64_t q0 = (int64_t)(x2 ? bt2 - tiles_a : bt2) * kK1Rows;
             if (q0 < cnt2) {
                 const int64_t nr2 = cnt2 - q0 < kK1Rows ? cnt2 - q0 : kK1Rows;
-                const uint64_t *g2 = (x2 ? prm.x_mag : prm.a_mag) + q0 * L;
+                const uint64_t *g2 = (x2 ? prm.x_mag + vb * prm.x_vstride * L : prm.a_mag) + q0 * L;
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g2),
                              "r"((unsigned)(nr2 * L * 8) & ~15u) : "memory");
             }
@@ -539,7 +540,8 @@ HK_DEV int k3_coef_of_limb(int qq, int w, int *sh) {
 // of Y (y = m 2^-P; canonical: sign 0 iff m = 0), Lr = L + 1 output limbs (|Y| / 2^P < n 2^P).
 // M: |Y| in Ly limbs (shared).  Block-wide: sticky bits, the first q limb that is not all ones
 // (where a rounding increment stops), and whether q is nonzero.
-HK_DEV void k3_store_rounded(const Params &prm, const uint64_t *M, bool neg, int64_t orow) {
+HK_DEV void k3_store_rounded(const Params &prm, const uint64_t *M, bool neg, int64_t orow,
+                             uint64_t *y_mag, int8_t *y_sign) {
     __shared__ int s_first;
     const int tid = threadIdx.x, T = blockDim.x, Ly = prm.Ly, Lr = prm.L + 1, P = prm.P;
     const int qs = P >> 6, qb = P & 63, hl = (P - 1) >> 6, hb = (P - 1) & 63;
@@ -562,14 +564,14 @@ HK_DEV void k3_store_rounded(const Params &prm, const uint64_t *M, bool neg, int
     const bool lsb = (M[qs] >> qb) & 1;
     const bool inc = half && (sticky || lsb);
     const int first = s_first;
-    uint64_t *yo = prm.y_mag + orow * Lr;
+    uint64_t *yo = y_mag + orow * Lr;
     for (int j = tid; j < Lr; j += T) {
         const uint64_t lo = qs + j < Ly ? M[qs + j] : 0, hi = qs + j + 1 < Ly ? M[qs + j + 1] : 0;
         uint64_t q = qb ? ((lo >> qb) | (hi << (64 - qb))) : lo;
         if (inc) q = j < first ? 0ull : (j == first ? q + 1 : q);
         yo[j] = q;
     }
-    if (tid == 0) prm.y_sign[orow] = (nz || inc) ? (neg ? (int8_t)-1 : (int8_t)1) : (int8_t)0;
+    if (tid == 0) y_sign[orow] = (nz || inc) ? (neg ? (int8_t)-1 : (int8_t)1) : (int8_t)0;
     __syncthreads();  // s_first reuse
 }
 
@@ -582,6 +584,10 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t r0 = prm.row0 + (int64_t)blockIdx.x * R;
     const int64_t m = prm.m;
+    const int64_t vb = (int64_t)blockIdx.y;  // batch vector (0 unless hk_matvec_prepared_batch)
+    const uint32_t *Yhat = prm.Yhat + vb * (int64_t)kNumPrimes * N2 * prm.ldY;
+    uint64_t *y_mag = prm.y_mag + vb * prm.y_vstride * (prm.round_out ? prm.L + 1 : prm.Ly);
+    int8_t *y_sign = prm.y_sign + vb * prm.y_vstride;
 
     // (0) Y^ columns of the R rows, all primes -> smem
     {
@@ -590,7 +596,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
             const int kp = e >> LOGN2, sg = e & (N2 - 1);
             const uint32_t *g;
             if (prm.shard_gamma == 0) {
-                g = prm.Yhat + (int64_t)(kp * N2 + sg) * prm.ldY + r0;
+                g = Yhat + (int64_t)(kp * N2 + sg) * prm.ldY + r0;
             } else {  // all-to-all receive buffer [source rank][prime][sigma-block column][rpr]
                 const int src = sg >> prm.log_n2loc, q = sg & (prm.n2loc - 1);  // rank src held block src
                 g = prm.Yhat + ((int64_t)(src * kNumPrimes + kp) * prm.n2loc + q) * prm.shard_rpr +
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
         const int nr = (int)(m - r0 < R ? m - r0 : R);
         const int ndst = prm.p2p ? (1 << prm.shard_gamma) : 1;  // peer memory: every rank's y
         for (int d = 0; d < ndst; ++d) {
-            uint64_t *ybase = prm.p2p ? prm.peer_ymag[d] : prm.y_mag;
+            uint64_t *ybase = prm.p2p ? prm.peer_ymag[d] : y_mag;
             int rr = 0, l = tid;
             while (l >= Ly) { l -= Ly; ++rr; }
             auto row_ptr = [&](int q) {
@@ -927,7 +933,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
             if (tid < nr) {
                 const int64_t o = r0 + tid;
                 const int64_t orow = prm.reverse_out ? (prm.y_rows - 1 - o) : o;
-                (prm.p2p ? prm.peer_ysign[d] : prm.y_sign)[orow] =
+                (prm.p2p ? prm.peer_ysign[d] : y_sign)[orow] =
                     s_neg[tid] ? (int8_t)-1 : (s_zmin[tid] < Ly ? (int8_t)1 : (int8_t)0);
             }
         }
@@ -935,7 +941,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
         for (int rr = 0; rr < R && r0 + rr < m; ++rr) {
             const int64_t o = r0 + rr;
             k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0,
-                             prm.reverse_out ? (prm.y_rows - 1 - o) : o);
+                             prm.reverse_out ? (prm.y_rows - 1 - o) : o, y_mag, y_sign);
         }
     }
 #else
@@ -948,12 +954,12 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
             // peer-memory exchange: the y all-gather fused into the stores (every rank's y buffer)
             const int ndst = prm.p2p ? (1 << prm.shard_gamma) : 1;
             for (int d = 0; d < ndst; ++d) {
-                uint64_t *yo = (prm.p2p ? prm.peer_ymag[d] : prm.y_mag) + orow * Ly;
+                uint64_t *yo = (prm.p2p ? prm.peer_ymag[d] : y_mag) + orow * Ly;
                 for (int l = tid; l < Ly; l += T) yo[l] = ybuf[rr * Ly + l];
-                if (tid == 0) (prm.p2p ? prm.peer_ysign[d] : prm.y_sign)[orow] = sgn;
+                if (tid == 0) (prm.p2p ? prm.peer_ysign[d] : y_sign)[orow] = sgn;
             }
         } else {
-            k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0, orow);
+            k3_store_rounded(prm, ybuf + (size_t)rr * Ly, s_neg[rr] != 0, orow, y_mag, y_sign);
         }
     }
 #endif
@@ -994,7 +1000,7 @@ static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int nti
     if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2, GAMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem1) != cudaSuccess)
         return HK_ECUDA;
-    k1_slice_rowntt<LOGN2, GAMMA><<<ntiles, k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
+    k1_slice_rowntt<LOGN2, GAMMA><<<dim3((unsigned)ntiles, (unsigned)prm.nvec), k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();
 }
 
@@ -1060,7 +1066,7 @@ int launch_ntt_path(const Params &prm, void *stream, uint32_t stages) {
 
 template <int LOGN1, int MODE>
 static int launch_cols_mode(const Params &prm, cudaStream_t st) {
-    const int ncols = kNumPrimes * prm.n2loc;
+    const int ncols = kNumPrimes * prm.n2loc * (MODE == 2 ? prm.nvec : 1);
     const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
     if (cudaFuncSetAttribute(k2_column<LOGN1, TwGlobal, MODE>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1115,7 +1121,7 @@ static int launch_k3(const Params &prm, cudaStream_t st, int64_t nrows) {
                              (int)smem) != cudaSuccess)
         return HK_ECUDA;
     const unsigned grid = (unsigned)((nrows + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
-    k3_finish<LOGN2, CH><<<grid, k3_threads<LOGN2>(), smem, st>>>(prm);
+    k3_finish<LOGN2, CH><<<dim3(grid, (unsigned)prm.nvec), k3_threads<LOGN2>(), smem, st>>>(prm);
     return check_launch();
 }
 

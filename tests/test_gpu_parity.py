@@ -525,3 +525,31 @@ def test_circulant_w64_plan(hk):
     rows = np.array([0, 12345, n - 1])
     wm, ws_ = oracle.matvec(2, P, am, asg, xm, xsg, rows=rows)
     assert_same((gm[rows], gs[rows]), (wm, ws_), "w=64 circulant rows")
+
+
+# ---------------------------------------------------------------------------------------------
+# F1 kernel-level batch (hk_matvec_prepared_batch): one launch per kernel for several vectors
+@pytest.mark.parametrize("kind,n,P,batch", [(0, 300, 5000, 3), (1, 77, 3328, 2), (2, 128, 1000, 4),
+                                            (2, 77, 700, 3), (0, 8200, 64, 2)])
+def test_prepared_batch_kernel_level(hk, kind, n, P, batch):
+    am, asg, _, _ = gen.make_inputs(kind, n, P, seed=61 + n)
+    A = hk.PreparedMatrix(kind, *hk.to_device(am, asg), P, n, batch=batch)
+    xs_host = [gen.uniform(400 + v, 1, n, P) for v in range(2 * batch + 1)]
+    ys = A.matvec_batch([hk.to_device(xm, xsg) for xm, xsg in xs_host])  # batch-size groups + a remainder
+    for v, ((xm, xsg), y) in enumerate(zip(xs_host, ys)):
+        assert_same(hk.to_host(*y), oracle.matvec(kind, P, am, asg, xm, xsg),
+                    f"kernel batch kind={kind} n={n} v={v}")
+    # the stacked call directly, and a rejected vector inside a batch
+    xm = torch.stack([hk.to_device(*xs_host[v])[0] for v in range(batch)])
+    xsg = torch.stack([hk.to_device(*xs_host[v])[1] for v in range(batch)])
+    if (n * gen.n_limbs(P)) % 2:  # vector 1 would start 8-byte aligned: the ABI rejects it
+        with pytest.raises(hk.HKError):
+            A.matvec_stacked(xm, xsg)
+        return
+    ym, ysg = A.matvec_stacked(xm, xsg)
+    for v in range(batch):
+        assert_same(hk.to_host(ym[v], ysg[v]), oracle.matvec(kind, P, am, asg, *xs_host[v]), f"stacked v={v}")
+    bad = xsg.clone()
+    bad[batch - 1, 0] = 2  # a sign outside {-1, 0, 1}
+    with pytest.raises(hk.HKError):
+        A.matvec_stacked(xm, bad)

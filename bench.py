@@ -104,6 +104,13 @@ def workload(cfg_name):
                      f"{c['recipe']}")
 
 
+def workload_config(wl):
+    """The `config` object, identical for both arms (the workload, and the L2 note the contract asks for)."""
+    return {"workload": wl["desc"], "kind": gen.KIND_NAMES[wl["kind"]], "n": wl["n"], "P": wl["P"],
+            "l2": "no flush: every step streams its own inputs and transform-domain arrays (C3: 100 MB of "
+                  "inputs + 1.48 GB of transform-domain traffic), far beyond the 126 MB L2"}
+
+
 def alg_counts(plan, m=None):
     """Algorithmic operation counts per matvec: full transforms, no
     pruning credit."""
@@ -273,7 +280,7 @@ def run_reference(args, wl, rank, world):
             "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": wl["desc"]},
+            "config": workload_config(wl),
             "cpu_baseline": {**cb, "value": value},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t_all}
@@ -801,17 +808,14 @@ def main():
         "warmup": W, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded SplitMix64 mantissas, BASELINE configs recipe)",
-        "config": {"workload": wl["desc"], "kind": gen.KIND_NAMES[kind], "n": n, "P": P,
-                   "plan": {k: plan[k] for k in ("w", "Ls", "log_n1", "log_n2", "k_primes",
-                                                 "margin_bits")},
-                   "parallelism": "single GPU" if world == 1 else (
-                       (f"sigma-coset x{world}: " + ("exchanges fused into K2/K3 stores over peer memory "
-                                                     "(symmetric memory, NVLink) + device barriers"
-                                                     if getattr(sh, "p2p", False) else
-                                                     "NCCL all-to-all + all-gather"))
-                       if args.plan == "coset" else f"row-block x{world} + NCCL all-gather"),
-                   "l2": "no flush: per-step working set (inputs 100 MB + transform-domain "
-                         f"{all_bytes / 1e6:.0f} MB traffic) exceeds the 126 MB L2"},
+        "config": workload_config(wl),
+        "plan": {k: plan[k] for k in ("w", "Ls", "log_n1", "log_n2", "k_primes", "margin_bits")},
+        "parallelism": "single GPU" if world == 1 else (
+            (f"sigma-coset x{world}: " + ("exchanges fused into K2/K3 stores over peer memory "
+                                          "(symmetric memory, NVLink) + device barriers"
+                                          if getattr(sh, "p2p", False) else
+                                          "NCCL all-to-all + all-gather"))
+            if args.plan == "coset" else f"row-block x{world} + NCCL all-gather"),
         "stages_ms": dict(zip(stage_names, stage_ms)),
         "roofline": roof,
         "verification": verification,

@@ -21,9 +21,9 @@
 //            128-bit sum of the coefficients whose bit offset falls in it, then the binary carry
 //            lookahead of K3 v2 and -Cb sum_s 2^(w s) added limb by limb (table in the workspace).
 //
-// Scope: N2 <= 8192, N1 <= 32768 -- every BASELINE config.  N1 <= 4096: a column pair of a and x
-// in shared memory per CTA (F2); N1 = 2^(12+g): the first g forward and last g inverse column stages
-// run from HBM (f2_top / f2_bottom) around 4096-point blocks in shared memory.  The NTT path stays
+// Scope: N2 <= 8192, N1 <= 32768 -- every BASELINE config.  N1 <= 2048: the a and x columns in
+// shared memory per CTA (F2); N1 = 2^(11+g): the first g forward and last g inverse column stages
+// run from HBM (f2_top / f2_bottom) around 2048-point blocks in shared memory (2 CTAs per SM).  The NTT path stays
 // the product headline (this one moves complex doubles: ~20 GB of HBM traffic per C3 matvec).
 #include <cuda_runtime.h>
 
@@ -80,6 +80,10 @@ __device__ __forceinline__ double2 cmulc(double2 a, double2 w) {  // a * conj(w)
                         __dsub_rn(__dmul_rn(a.y, w.x), __dmul_rn(a.x, w.y)));
 }
 __host__ __device__ __forceinline__ int cpad(int i) { return i + (i >> 3); }  // shared-memory padding
+__device__ __forceinline__ void fcp_async16(double2 *smem, const double2 *gmem) {  // LDGSTS, 16 bytes
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 
 // One radix-2^R pass over `batch` arrays of N = 2^LOGN points (array b at s + b * rs, point i at
 // cpad(i)).  DIF (INV = false): stages h = S 2^(R-1) .. S, (u, v) -> (u + v, (u - v) w);
@@ -204,22 +208,25 @@ __global__ void __launch_bounds__(kFftThreads) f1_rows(FftParams prm) {
 
 // F2: per pair of columns: forward column FFTs (N1) of a and x, pointwise product, inverse FFT;
 // the result replaces x's columns (all N1 rows)
-// SPLIT (N1 > 2^LOGN1 = 4096): block blockIdx.y of 4096 consecutive rows after f2_top's first
-// stages; the block is then an independent 4096-point transform (its stages' twiddles are the
-// N1 table's first 4096 entries) and every row holds data (no zero masking)
+// SPLIT (N1 > 2^LOGN1 = 2048): block blockIdx.y of 2048 consecutive rows after f2_top's first
+// stages; the block is then an independent 2048-point transform (its stages' twiddles are the
+// N1 table's first 2048 entries) and every row holds data (no zero masking)
+constexpr int kF2Threads = 256, kF2LogBlock = 11;  // F2: 2048-row blocks, 2 CTAs (74 KB smem) per SM
 template <int LOGN1, int TC, bool SPLIT>
-__global__ void __launch_bounds__(kFftThreads) f2_cols(FftParams prm) {
+__global__ void __launch_bounds__(kF2Threads, 2) f2_cols(FftParams prm) {
     constexpr int N1 = 1 << LOGN1, RS = N1 + N1 / 8;
     extern __shared__ double2 cs[];  // [2 arrays][TC columns][RS]
     const int sig0 = blockIdx.x * TC, N2 = prm.N2;
     const int64_t na = SPLIT ? N1 : prm.a_count, nx = SPLIT ? N1 : prm.n;
     const size_t row0 = SPLIT ? (size_t)blockIdx.y * N1 : 0;
-    for (int e = threadIdx.x; e < N1 * TC; e += blockDim.x) {
+    for (int e = threadIdx.x; e < N1 * TC; e += blockDim.x) {  // asynchronous 16-byte copies
         const int i = e / TC, c = e % TC;
         const size_t g = (row0 + i) * N2 + sig0 + c;
-        cs[c * RS + cpad(i)] = i < na ? prm.A[g] : make_double2(0.0, 0.0);
-        cs[(TC + c) * RS + cpad(i)] = i < nx ? prm.X[g] : make_double2(0.0, 0.0);
+        double2 *da = &cs[c * RS + cpad(i)], *dx = &cs[(TC + c) * RS + cpad(i)];
+        if (i < na) fcp_async16(da, prm.A + g); else *da = make_double2(0.0, 0.0);
+        if (i < nx) fcp_async16(dx, prm.X + g); else *dx = make_double2(0.0, 0.0);
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     CDif<LOGN1, LOGN1>::run(cs, 2 * TC, RS, prm.tw1);
     for (int e = threadIdx.x; e < N1 * TC; e += blockDim.x) {
@@ -235,11 +242,11 @@ __global__ void __launch_bounds__(kFftThreads) f2_cols(FftParams prm) {
     }
 }
 
-// N1 = 2^(12 + GAMMA) > 4096: the first GAMMA forward stages (half-sizes N1/2 .. 4096) of the a and
-// x columns from HBM, in place; thread item = (array, j0 < 4096, sigma), sigma fastest (coalesced)
+// N1 = 2^(11 + GAMMA) > 2048: the first GAMMA forward stages (half-sizes N1/2 .. 2048) of the a and
+// x columns from HBM, in place; thread item = (array, j0 < 2048, sigma), sigma fastest (coalesced)
 template <int GAMMA>
 __global__ void __launch_bounds__(256) f2_top(FftParams prm) {
-    constexpr int G = 1 << GAMMA, S = 4096;
+    constexpr int G = 1 << GAMMA, S = 1 << kF2LogBlock;
     const int N2 = prm.N2;
     const int64_t items = (int64_t)2 * S * N2;
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -276,7 +283,7 @@ __global__ void __launch_bounds__(256) f2_top(FftParams prm) {
 // ... and the last GAMMA inverse stages (half-sizes 4096 .. N1/2) of the product, in place
 template <int GAMMA>
 __global__ void __launch_bounds__(256) f2_bottom(FftParams prm) {
-    constexpr int G = 1 << GAMMA, S = 4096;
+    constexpr int G = 1 << GAMMA, S = 1 << kF2LogBlock;
     const int N2 = prm.N2;
     const int64_t items = (int64_t)S * N2;
     for (int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; it < items;
@@ -320,7 +327,8 @@ __global__ void __launch_bounds__(kFftThreads) f3_finish(FftParams prm) {
     for (int rep = 0; rep < nrep; ++rep) {
         const int64_t pos = (prm.out_off + i + (rep ? prm.n : 0)) & (N1 - 1);
         const double2 *src = prm.X + pos * N2;
-        for (int t = tid; t < N2; t += T) cs[cpad(t)] = src[t];
+        for (int t = tid; t < N2; t += T) fcp_async16(&cs[cpad(t)], src + t);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         CDit<LOGN2, 0>::run(cs, 1, 0, prm.tw2);
         for (int t = tid; t < N2; t += T) {
@@ -592,19 +600,19 @@ int launch_rows_fft(const FftParams &prm, cudaStream_t st) {
 }
 template <int LOGN1>
 int launch_cols_fft(const FftParams &prm, cudaStream_t st) {
-    constexpr bool SPLIT = LOGN1 > 12;
-    constexpr int LB = SPLIT ? 12 : LOGN1, TC = LB >= 12 ? 1 : 2;
+    constexpr bool SPLIT = LOGN1 > kF2LogBlock;
+    constexpr int LB = SPLIT ? kF2LogBlock : LOGN1, TC = LB >= kF2LogBlock ? 1 : 2;
     const size_t sm = (size_t)2 * TC * ((1 << LB) + (1 << LB) / 8) * sizeof(double2);
     if (cudaFuncSetAttribute(f2_cols<LB, TC, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
         return HK_ECUDA;
-    constexpr int GAMMA = SPLIT ? LOGN1 - 12 : 0;
+    constexpr int GAMMA = SPLIT ? LOGN1 - kF2LogBlock : 0;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     if constexpr (SPLIT) {
         f2_top<GAMMA><<<(unsigned)(nsm * 8), 256, 0, st>>>(prm);
         if (const int rc = fft_check_launch()) return rc;
     }
-    f2_cols<LB, TC, SPLIT><<<dim3((unsigned)(prm.N2 / TC), 1u << GAMMA), kFftThreads, sm, st>>>(prm);
+    f2_cols<LB, TC, SPLIT><<<dim3((unsigned)(prm.N2 / TC), 1u << GAMMA), kF2Threads, sm, st>>>(prm);
     if (const int rc = fft_check_launch()) return rc;
     if constexpr (SPLIT) {
         f2_bottom<GAMMA><<<(unsigned)(nsm * 8), 256, 0, st>>>(prm);

@@ -219,6 +219,12 @@ typedef struct {
     int64_t chunk_words;    /* uint32 words per all-to-all chunk = 5 block_cols rpr             */
     int64_t buffer_words;   /* send / recv buffer words = G chunk_words                        */
     uint64_t ws_bytes;      /* per-rank workspace bytes                                         */
+    /* sliced sharding (hk_hankel_shard_slice / _columns below); 0 when unsupported (N1 > 2^14 or
+     * fewer than 8 matrix positions per rank)                                                     */
+    int64_t slice_chunk_words;   /* words per (source, destination) slice chunk                  */
+    int64_t slice_buffer_words;  /* slice send / receive buffer words = G slice_chunk_words      */
+    int64_t slice_rows_a;        /* matrix positions of a (and of x) each rank slices: ldA / G   */
+    int64_t slice_rows_x;        /*   and ldX / G                                                */
 } hk_shard_info;
 
 int32_t hk_shard_plan(int32_t kind, int64_t n, int32_t P, int32_t G, hk_shard_info *out);
@@ -233,6 +239,37 @@ int32_t hk_hankel_shard_forward(int32_t kind, int64_t n, int32_t P, int32_t G, i
 int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
                                const uint32_t *recv, uint64_t *y_mag, int8_t *y_sign, void *ws,
                                size_t ws_bytes, void *stream);
+
+/* SLICED sharding (round 2): hk_hankel_shard_forward slices EVERY entry on every rank (its slicing
+ * and residues are replicated); this variant splits it too.  Phase 1a, rank g,
+ * hk_hankel_shard_slice: slices only the entries at matrix positions [g Rs, (g+1) Rs) of a and of x
+ * (Rs = slice_rows_a / slice_rows_x; x positions are reversed rows for Hankel / Toeplitz), runs the
+ * full slice transform and scatters block d of its outputs into chunk d of `slice_send`:
+ * [dest d][a part: prime][column of block d][Rs_a] then [x part: prime][column][Rs_x]; positions
+ * past the entry counts are never written (keep the buffer zero-initialised).  An all-to-all of the
+ * slice chunks follows.  Phase 1b, hk_hankel_shard_columns: with `slice_recv` = [source s][...]
+ * (source s's positions), the matrix-index transforms of rank g's columns, exactly as
+ * hk_hankel_shard_forward's second half, into `send`.  Phase 2 is hk_hankel_shard_finish.
+ * The data-status word of a rank covers the entries it sliced: all-reduce the ranks' status. */
+int32_t hk_hankel_shard_slice(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                              const uint64_t *a_mag, const int8_t *a_sign,
+                              const uint64_t *x_mag, const int8_t *x_sign, uint32_t *slice_send,
+                              void *ws, size_t ws_bytes, void *stream);
+int32_t hk_hankel_shard_columns(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                const uint32_t *slice_recv, uint32_t *send, void *ws,
+                                size_t ws_bytes, void *stream);
+/* ... and with the slice exchange fused into K1's stores over peer memory: slice_recv_ptrs[d] = rank
+ * d's slice receive buffer (this rank writes chunk g of it); a system-scope fence ends the kernel,
+ * the caller barriers before phase 1b; hk_hankel_shard_columns_p2p then stores its row-block chunks
+ * straight into the ranks' receive buffers as hk_hankel_shard_forward_p2p does. */
+int32_t hk_hankel_shard_slice_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                  const uint64_t *a_mag, const int8_t *a_sign,
+                                  const uint64_t *x_mag, const int8_t *x_sign,
+                                  uint32_t *const *slice_recv_ptrs, void *ws, size_t ws_bytes,
+                                  void *stream);
+int32_t hk_hankel_shard_columns_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                    const uint32_t *slice_recv, uint32_t *const *recv_ptrs,
+                                    void *ws, size_t ws_bytes, void *stream);
 
 /* The same two phases with the collectives fused into the kernels' stores over peer memory
  * (NVLink / NVSwitch P2P; pointers mapped into this process, e.g. torch symmetric memory):

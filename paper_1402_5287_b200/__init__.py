@@ -72,7 +72,9 @@ class ShardInfo(ctypes.Structure):
     _fields_ = [("G", ctypes.c_int32), ("gamma", ctypes.c_int32), ("block_cols", ctypes.c_int64),
                 ("rows_per_rank", ctypes.c_int64), ("y_rows", ctypes.c_int64),
                 ("chunk_words", ctypes.c_int64), ("buffer_words", ctypes.c_int64),
-                ("ws_bytes", ctypes.c_uint64)]
+                ("ws_bytes", ctypes.c_uint64), ("slice_chunk_words", ctypes.c_int64),
+                ("slice_buffer_words", ctypes.c_int64), ("slice_rows_a", ctypes.c_int64),
+                ("slice_rows_x", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -112,6 +114,10 @@ def _load():
         "hk_hankel_shard_finish_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, sz, vp]),
         "hk_matvec_prepared": (i32, [i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp]),
         "hk_karatsuba_matvec": (i32, [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_slice": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_slice_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_columns": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, sz, vp]),
+        "hk_hankel_shard_columns_p2p": (i32, [i32, i64, i32, i32, i32, vp, vp, vp, sz, vp]),
         "hk_batch_workspace_size": (i32, [i32, i64, i64, i32, i32, ctypes.POINTER(sz)]),
         "hk_batch_workspace_init": (i32, [i32, i64, i64, i32, i32, vp, sz, vp]),
         "hk_matvec_prepared_batch": (i32, [i32, i64, i64, i32, i32, vp, vp, vp, vp, vp, sz, vp]),
@@ -135,7 +141,8 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_shard_workspace_init", "hk_hankel_shard_forward", "hk_hankel_shard_finish",
             "hk_matvec_rounded", "hk_hankel_shard_forward_p2p", "hk_hankel_shard_finish_p2p",
             "hk_fft_plan", "hk_fft_workspace_init", "hk_fft_matvec", "hk_batch_workspace_size",
-            "hk_batch_workspace_init", "hk_matvec_prepared_batch")
+            "hk_batch_workspace_init", "hk_matvec_prepared_batch", "hk_hankel_shard_slice",
+            "hk_hankel_shard_slice_p2p", "hk_hankel_shard_columns", "hk_hankel_shard_columns_p2p")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -453,6 +460,58 @@ def shard_forward(ws: ShardWorkspace, g, a_mag, a_sign, x_mag, x_sign, send, str
             _dev_ptr(send, (torch.int32,), (ws.info["buffer_words"],), "send")]
     _check(_lib.hk_hankel_shard_forward(ws.kind, ws.n, ws.P, ws.G, int(g), *ptrs, ws.ptr,
                                         ws.nbytes, _stream_ptr(stream)), "hk_hankel_shard_forward")
+
+
+def shard_slice(ws: ShardWorkspace, g, a_mag, a_sign, x_mag, x_sign, slice_send, stream=None):
+    """Sliced phase 1a of rank g: K1 over this rank's matrix positions only, every sigma-block
+    scattered into chunk d of slice_send (int32, slice_buffer_words, zero-initialised)."""
+    import torch
+    L, na = limbs(ws.P), (ws.n if ws.kind == CIRCULANT else 2 * ws.n - 1)
+    ptrs = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (ws.n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (ws.n,), "x_sign"),
+            _dev_ptr(slice_send, (torch.int32,), (ws.info["slice_buffer_words"],), "slice_send")]
+    _check(_lib.hk_hankel_shard_slice(ws.kind, ws.n, ws.P, ws.G, int(g), *ptrs, ws.ptr, ws.nbytes,
+                                      _stream_ptr(stream)), "hk_hankel_shard_slice")
+
+
+def shard_slice_p2p(ws: ShardWorkspace, g, a_mag, a_sign, x_mag, x_sign, slice_recv_ptrs, stream=None):
+    """Sliced phase 1a with the slice exchange fused into K1's stores: slice_recv_ptrs[d] = rank d's
+    slice receive buffer (peer memory)."""
+    import torch
+    L, na = limbs(ws.P), (ws.n if ws.kind == CIRCULANT else 2 * ws.n - 1)
+    if len(slice_recv_ptrs) != ws.G:
+        raise ValueError("need one slice receive-buffer pointer per rank")
+    ptrs = [_dev_ptr(a_mag, _mag_dtypes(), (na, L), "a_mag"),
+            _dev_ptr(a_sign, (torch.int8,), (na,), "a_sign"),
+            _dev_ptr(x_mag, _mag_dtypes(), (ws.n, L), "x_mag"),
+            _dev_ptr(x_sign, (torch.int8,), (ws.n,), "x_sign")]
+    arr = _ptr_array(slice_recv_ptrs)
+    _check(_lib.hk_hankel_shard_slice_p2p(ws.kind, ws.n, ws.P, ws.G, int(g), *ptrs,
+                                          ctypes.cast(arr, ctypes.c_void_p), ws.ptr, ws.nbytes,
+                                          _stream_ptr(stream)), "hk_hankel_shard_slice_p2p")
+
+
+def shard_columns(ws: ShardWorkspace, g, slice_recv, send, stream=None):
+    """Sliced phase 1b of rank g: K2 on its columns gathered from slice_recv; output into send."""
+    import torch
+    r = _dev_ptr(slice_recv, (torch.int32,), (ws.info["slice_buffer_words"],), "slice_recv")
+    sd = _dev_ptr(send, (torch.int32,), (ws.info["buffer_words"],), "send")
+    _check(_lib.hk_hankel_shard_columns(ws.kind, ws.n, ws.P, ws.G, int(g), r, sd, ws.ptr, ws.nbytes,
+                                        _stream_ptr(stream)), "hk_hankel_shard_columns")
+
+
+def shard_columns_p2p(ws: ShardWorkspace, g, slice_recv, recv_ptrs, stream=None):
+    """Sliced phase 1b with the all-to-all fused into K2's stores (recv_ptrs[d] = rank d's receive buffer)."""
+    import torch
+    if len(recv_ptrs) != ws.G:
+        raise ValueError("need one receive-buffer pointer per rank")
+    r = _dev_ptr(slice_recv, (torch.int32,), (ws.info["slice_buffer_words"],), "slice_recv")
+    arr = _ptr_array(recv_ptrs)
+    _check(_lib.hk_hankel_shard_columns_p2p(ws.kind, ws.n, ws.P, ws.G, int(g), r,
+                                            ctypes.cast(arr, ctypes.c_void_p), ws.ptr, ws.nbytes,
+                                            _stream_ptr(stream)), "hk_hankel_shard_columns_p2p")
 
 
 def shard_finish(ws: ShardWorkspace, g, recv, y_mag, y_sign, stream=None):

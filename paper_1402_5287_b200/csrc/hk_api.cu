@@ -190,6 +190,13 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     // K2 is split)
     if (!pl->split_k2) pl->off_AT = pl->off_end;
     pl->off_end_prepared = pl->split_k2 ? pl->off_end : align256(pl->off_AT + at_bytes);
+    if (G > 1) {  // sliced sharding: each rank slices ldA / G positions of a and ldX / G of x
+        pl->rs_a = pl->ldA / G;
+        pl->rs_x = pl->ldX / G;
+        pl->slice_ok = in.log_n1 <= 14 && pl->rs_a >= 8 && pl->rs_x >= 8 &&
+                       (pl->rs_a & (pl->rs_a - 1)) == 0 && (pl->rs_x & (pl->rs_x - 1)) == 0;
+        pl->slice_chunk = (int64_t)kNumPrimes * N2loc * (pl->rs_a + pl->rs_x);
+    }
     pl->xhat_bytes = align256((size_t)kNumPrimes * N2loc * pl->ldX * 4);
     pl->yhat_bytes = align256((size_t)kNumPrimes * N2 * pl->ldY * 4);
     in.ws_bytes = pl->off_end;
@@ -770,6 +777,10 @@ int32_t hk_shard_plan(int32_t kind, int64_t n, int32_t P, int32_t G, hk_shard_in
     out->chunk_words = (int64_t)kNumPrimes * out->block_cols * pl.rpr;
     out->buffer_words = (int64_t)G * out->chunk_words;
     out->ws_bytes = pl.info.ws_bytes;
+    out->slice_chunk_words = pl.slice_ok ? pl.slice_chunk : 0;
+    out->slice_buffer_words = pl.slice_ok ? (int64_t)G * pl.slice_chunk : 0;
+    out->slice_rows_a = pl.slice_ok ? pl.rs_a : 0;
+    out->slice_rows_x = pl.slice_ok ? pl.rs_x : 0;
     return HK_OK;
 }
 
@@ -828,6 +839,117 @@ int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, in
     const int64_t row0 = prm.shard_row0;
     const int64_t nrows = (n - row0) < pl.rpr ? (n - row0) : pl.rpr;
     return launch_k3_range(prm, stream, row0, nrows);
+}
+
+// ---- sliced sharding: phase 1a (K1 over this rank's positions, scatter) and 1b (K2 gathers)
+static int slice_common(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g, void *ws,
+                        size_t ws_bytes, Plan *pl, Params *prm) {
+    int rc = shard_common(kind, n, P, G, g, ws, ws_bytes, pl, prm);
+    if (rc) return rc;
+    if (!pl->slice_ok) return HK_EUNSUPPORTED;
+    prm->slice_mode = 1;
+    int lg = 0;
+    while ((int64_t(1) << lg) < pl->rs_a) ++lg;
+    prm->lg_rs_a = lg;
+    lg = 0;
+    while ((int64_t(1) << lg) < pl->rs_x) ++lg;
+    prm->lg_rs_x = lg;
+    prm->slice_chunk = pl->slice_chunk;
+    prm->slice_xoff = (int64_t)kNumPrimes * prm->n2loc * pl->rs_a;
+    return HK_OK;
+}
+
+// K1 tiles covering matrix positions [g Rs, (g+1) Rs) of a, then of x (x positions are reversed
+// rows for Hankel / Toeplitz); tiles straddling two ranks' ranges are run by both, each storing
+// its own positions only
+static int launch_slice_k1(const Plan &pl, const Params &prm, int32_t g, void *stream) {
+    const int kT = k1_tile_rows();
+    const int ga = k1_tiles_a(prm), gx = k1_tiles_x(prm);
+    const int64_t na = pl.info.a_count, n = pl.info.n;
+    int64_t lo = (int64_t)g * pl.rs_a, hi = lo + pl.rs_a < na ? lo + pl.rs_a : na;
+    int rc;
+    if (hi > lo) {
+        const int t0 = (int)(lo / kT), t1 = (int)((hi + kT - 1) / kT);
+        if ((rc = launch_k1_range(prm, stream, t0, t1 - t0))) return rc;
+    }
+    lo = (int64_t)g * pl.rs_x;
+    hi = lo + pl.rs_x < n ? lo + pl.rs_x : n;
+    if (hi > lo) {
+        const int64_t r_lo = pl.x_reversed ? n - hi : lo, r_hi = pl.x_reversed ? n - lo : hi;
+        const int t0 = (int)(r_lo / kT), t1 = (int)((r_hi + kT - 1) / kT);
+        if ((rc = launch_k1_range(prm, stream, ga + t0, t1 - t0))) return rc;
+    }
+    (void)gx;
+    return HK_OK;
+}
+
+int32_t hk_hankel_shard_slice(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                              const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
+                              const int8_t *x_sign, uint32_t *slice_send, void *ws, size_t ws_bytes,
+                              void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !slice_send) return HK_EINVAL;
+    if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = slice_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
+    prm.slice_out = slice_send;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    return launch_slice_k1(pl, prm, g, stream);
+}
+
+int32_t hk_hankel_shard_slice_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                  const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
+                                  const int8_t *x_sign, uint32_t *const *slice_recv_ptrs, void *ws,
+                                  size_t ws_bytes, void *stream) {
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !slice_recv_ptrs) return HK_EINVAL;
+    if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = slice_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    for (int d = 0; d < G; ++d) {
+        if (!slice_recv_ptrs[d]) return HK_EINVAL;
+        prm.peer_slice[d] = slice_recv_ptrs[d];
+    }
+    prm.p2p = 1;
+    prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
+    if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), (cudaStream_t)stream) != cudaSuccess)
+        return HK_ECUDA;
+    return launch_slice_k1(pl, prm, g, stream);
+}
+
+int32_t hk_hankel_shard_columns(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                const uint32_t *slice_recv, uint32_t *send, void *ws, size_t ws_bytes,
+                                void *stream) {
+    if (!slice_recv || !send) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = slice_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    prm.slice_in = slice_recv;
+    prm.Yhat = send;
+    return launch_k2_sliced(prm, stream);
+}
+
+int32_t hk_hankel_shard_columns_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
+                                    const uint32_t *slice_recv, uint32_t *const *recv_ptrs, void *ws,
+                                    size_t ws_bytes, void *stream) {
+    if (!slice_recv || !recv_ptrs) return HK_EINVAL;
+    Plan pl;
+    Params prm;
+    int rc = slice_common(kind, n, P, G, g, ws, ws_bytes, &pl, &prm);
+    if (rc) return rc;
+    for (int d = 0; d < G; ++d) {
+        if (!recv_ptrs[d]) return HK_EINVAL;
+        prm.peer_recv[d] = recv_ptrs[d];
+    }
+    prm.p2p = 1;
+    prm.slice_in = slice_recv;
+    prm.Yhat = recv_ptrs[g];
+    return launch_k2_sliced(prm, stream);
 }
 
 int32_t hk_hankel_shard_forward_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,

@@ -104,6 +104,15 @@ struct Params {
     GarnerConsts gc;
     Garner2Consts g2;
     const uint64_t *negK;        // Ly limbs of -K mod 2^(64 Ly) (K3 v2), in the workspace
+    // sliced sharding: K1 slices only this rank's matrix positions [k1_block Rs, (k1_block+1) Rs)
+    // and scatters every sigma-block to its destination chunk; K2 gathers its columns from the
+    // slice receive buffer [source][a part | x part]
+    int32_t slice_mode;
+    int32_t lg_rs_a, lg_rs_x;    // log2 Rs of a and x
+    int64_t slice_chunk, slice_xoff;  // words per chunk, words of a chunk's a part
+    uint32_t *slice_out;         // K1: send buffer [dest][chunk] (NCCL layout)
+    uint32_t *peer_slice[kMaxShards];  // K1 p2p: rank d's slice receive buffer
+    const uint32_t *slice_in;    // K2: this rank's slice receive buffer [source][chunk]
     // F1 kernel-level batch (hk_matvec_prepared_batch): nvec vectors per launch; vector v's x / y
     // are x_vstride / y_vstride entries after vector v - 1's, its X^ / Y^ columns continue the
     // column index (X^ column c of vector v = column v * ncols + c, likewise Y^); 1 otherwise
@@ -125,6 +134,8 @@ struct Plan {
     size_t off_AT, off_end_prepared;
     size_t xhat_bytes, yhat_bytes;   // one vector's X^ / Y^ region (batch workspaces append nvec of each)
     int32_t split_k2;            // N1 >= 2^kSplitLogN1: AT inside the base layout, K2 in two launches
+    int32_t slice_ok;            // sliced sharding supported (G > 1, log_n1 <= 14, Rs >= 8)
+    int64_t rs_a, rs_x, slice_chunk;
 };
 
 // kernels (hk_ntt.cu)
@@ -137,6 +148,8 @@ int k1_tiles_a(const Params &prm);
 int k1_tiles_x(const Params &prm);
 int launch_k1_range(const Params &prm, void *stream, int tile0, int ntiles);
 int launch_k3_range(const Params &prm, void *stream, int64_t row0, int64_t nrows);
+// K2 of the sliced shards (columns gathered from the slice receive buffer)
+int launch_k2_sliced(const Params &prm, void *stream);
 // K2 variants: 0 = full (X^ and A^ transforms), 1 = prepare (A^ transform -> AT),
 // 2 = prepared (X^ transform x AT, inverse)
 int launch_k2_mode(const Params &prm, void *stream, int mode);

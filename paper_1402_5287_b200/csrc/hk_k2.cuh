@@ -98,6 +98,43 @@ HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, bool zu, ui
     else k2_dif_top_load<TW, LOGN, T, SRC_SMEM, false>(src, sm, tw, p);
 }
 
+// Sliced shards: the same top pass with the column gathered from the slice receive buffer, where
+// matrix position i of this column sits in source (i >> lg)'s chunk at offset i & (2^lg - 1).
+template <class TW, int LOGN, int T, bool ZU>
+HK_DEV void k2_dif_top_gather(const uint32_t *__restrict__ src, size_t chunk, int lg, uint32_t *sm,
+                              const uint2 *tw, uint32_t p) {
+    constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
+    const unsigned mask = (1u << lg) - 1u;
+    for (int j0 = threadIdx.x; j0 < S; j0 += T) {
+        uint32_t v[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) {
+            const unsigned i = (unsigned)(j0 + m * S);
+            if (ZU && m >= G / 2) v[m] = 0u;
+            else v[m] = __ldcs(src + (size_t)(i >> lg) * chunk + (i & mask));
+        }
+#pragma unroll
+        for (int l = R - 1; l >= 0; --l) {
+            const int half = 1 << l;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & half) continue;
+                if (ZU && l == R - 1) {  // (u, 0) -> (u, u W)
+                    const uint2 w = TW::ld(tw, S * half + j0 + S * m);
+                    v[m + half] = red1(shoup(v[m], w.x, w.y, p), p);
+                    continue;
+                }
+                const uint2 w = TW::ld(tw, S * half + j0 + S * (m & (half - 1)));
+                gs_bfly(v[m], v[m + half], w, p);
+            }
+        }
+        uint32_t *b0 = sm + pad(j0);
+#pragma unroll
+        for (int m = 0; m < G; ++m) b0[padded_len(m * S)] = v[m];
+    }
+    __syncthreads();
+}
+
 // Middle forward passes (R = 5), k = 1 .. NP-2.
 template <class TW, int LOGN, int K>
 struct K2DifMiddle {
@@ -219,7 +256,7 @@ constexpr size_t k2_smem_bytes() {
                                : (size_t)padded_len(1 << LOGN1) * 4 + (k2_smtw<LOGN1>() ? 16 + kK2LowTw * 8 : 0);
 }
 
-template <class TW, int LOGN1, bool SHARD>
+template <class TW, int LOGN1, bool SHARD, bool SLICED = false>
 HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, int kp, int sigma) {
     using PL = ColPlan<LOGN1>;
     constexpr int N1 = 1 << LOGN1, T = PL::T, RL = PL::RL, GL = PL::GL, GPT = PL::GPT;
@@ -228,11 +265,22 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     const uint32_t p = prm.pc[kp].p, pneg = prm.pc[kp].pneg;
     const size_t cidx = (size_t)kp * prm.n2loc + sigma;
     uint32_t *sA = sm + k2_stage_off<LOGN1>();
+    // sliced shards: this column's positions in the slice receive buffer (source 0's chunk)
+    const uint32_t *slA = SLICED ? prm.slice_in + (cidx << prm.lg_rs_a) : nullptr;
+    const uint32_t *slX = SLICED ? prm.slice_in + prm.slice_xoff + (cidx << prm.lg_rs_x) : nullptr;
     if constexpr (STAGE) {  // issue the A^ column copy now; consumed after X^'s transform
         const int nch = (int)prm.ldA >> 2;  // the zero-padded column (ldA = N1 or N1 / 2)
-        const uint32_t *g = prm.Ahat + cidx * prm.ldA;
-        for (int c = tid; c < nch; c += T) cp_async16(sA + 4 * c, g + 4 * c);
-    } else if (HK_K2_L2PF && tid == 0) {
+        if constexpr (SLICED) {  // 4-position segments never straddle two sources (Rs >= 8)
+            const unsigned mask = (1u << prm.lg_rs_a) - 1u;
+            for (int c = tid; c < nch; c += T) {
+                const unsigned i = 4u * c;
+                cp_async16(sA + i, slA + (size_t)(i >> prm.lg_rs_a) * prm.slice_chunk + (i & mask));
+            }
+        } else {
+            const uint32_t *g = prm.Ahat + cidx * prm.ldA;
+            for (int c = tid; c < nch; c += T) cp_async16(sA + 4 * c, g + 4 * c);
+        }
+    } else if (HK_K2_L2PF && !SLICED && tid == 0) {
         // no staging room: have the A^ column brought into L2 (bulk prefetch) during X^'s transform
         const uint32_t *g = prm.Ahat + cidx * prm.ldA;
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g),
@@ -256,7 +304,12 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
     // ---- X^: forward, bottom pass kept in registers
     {
         const int nx = (int)prm.n;
-        k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
+        if constexpr (SLICED) {
+            if (nx <= N1 / 2) k2_dif_top_gather<TW, LOGN1, T, true>(slX, prm.slice_chunk, prm.lg_rs_x, sm, twf, p);
+            else k2_dif_top_gather<TW, LOGN1, T, false>(slX, prm.slice_chunk, prm.lg_rs_x, sm, twf, p);
+        } else {
+            k2_dif_top_from_global<TW, LOGN1, T>(prm.Xhat + cidx * prm.ldX, nx <= N1 / 2, sm, twf, p);
+        }
         K2DifMiddle<TWM, LOGN1, 1>::run(sm, twm, p);
     }
     uint32_t xr[GPT][GL];
@@ -275,6 +328,9 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
             cp_async_wait_all();
             __syncthreads();
             k2_dif_top_from_global<TW, LOGN1, T, true>(sA, na <= N1 / 2, sm, twf, p);
+        } else if constexpr (SLICED) {
+            if (na <= N1 / 2) k2_dif_top_gather<TW, LOGN1, T, true>(slA, prm.slice_chunk, prm.lg_rs_a, sm, twf, p);
+            else k2_dif_top_gather<TW, LOGN1, T, false>(slA, prm.slice_chunk, prm.lg_rs_a, sm, twf, p);
         } else {
             k2_dif_top_from_global<TW, LOGN1, T>(prm.Ahat + cidx * prm.ldA, na <= N1 / 2, sm, twf, p);
         }
@@ -402,7 +458,7 @@ HK_DEV void k2_prepared_body(const Params &prm, uint32_t *sm, const uint2 *twf, 
 // One CTA per column; the N1 forward table is read through the read-only/L1 path.
 // MODE 0: full column (X^ and A^ transforms); 1: prepare A^ -> AT; 2: prepared (X^ x AT);
 // 3: full column of a sigma-coset shard (output to the all-to-all send buffer); 4: prepared column
-// of a shard.  N1 >= 2^15 runs MODE 1 then MODE 2 (4 for shards) instead of MODE 0 (3).
+// of a shard; 5: full column of a sliced shard (inputs gathered from the slice receive buffer).  N1 >= 2^15 runs MODE 1 then MODE 2 (4 for shards) instead of MODE 0 (3).
 template <int LOGN1, class TW = TwGlobal, int MODE = 0>
 __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k2_column(Params prm) {
     extern __shared__ uint32_t sm[];
@@ -415,6 +471,7 @@ __global__ void __launch_bounds__(k2_threads<LOGN1>(), k2_min_blocks<LOGN1>()) k
     const uint2 *twf = prm.tw + (size_t)kp * (prm.N2 + prm.N1) + prm.N2;
     if constexpr (MODE == 0) k2_column_body<TW, LOGN1, false>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 3) k2_column_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);
+    else if constexpr (MODE == 5) k2_column_body<TW, LOGN1, true, true>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 1) k2_prepare_body<TW, LOGN1>(prm, sm, twf, kp, sigma);
     else if constexpr (MODE == 2) k2_prepared_body<TW, LOGN1>(prm, sm, twf, kp, sigma, vb);
     else k2_prepared_body<TW, LOGN1, true>(prm, sm, twf, kp, sigma);

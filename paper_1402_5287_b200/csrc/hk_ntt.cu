@@ -322,14 +322,32 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
             const int64_t orow = r0 + rr;
             if (orow < count) {
                 const int64_t pos = rev ? (count - 1 - orow) : orow;
-                uint32_t *o = out + ((int64_t)kp * BL + (int64_t)g * GB) * ld + pos;
+                if (GAMMA == 0 && prm.slice_mode) {
+                    // sliced shards: positions [src Rs, (src+1) Rs) of this rank only; sigma-block
+                    // d = (g GB) / n2loc goes to chunk d of the send buffer (or, over peer memory,
+                    // to chunk src of rank d's receive buffer)
+                    const int lg = is_x ? prm.lg_rs_x : prm.lg_rs_a;
+                    const int64_t lo = (int64_t)prm.k1_block << lg;
+                    if (pos >= lo && pos < lo + (int64_t(1) << lg)) {
+                        const int sg0 = g * GB, dst = sg0 >> prm.log_n2loc, sl = sg0 & (prm.n2loc - 1);
+                        uint32_t *base = prm.p2p ? prm.peer_slice[dst] + (int64_t)prm.k1_block * prm.slice_chunk
+                                                 : prm.slice_out + (int64_t)dst * prm.slice_chunk;
+                        uint32_t *o = base + (is_x ? prm.slice_xoff : 0) + (((int64_t)kp * prm.n2loc + sl) << lg) +
+                                      (pos - lo);
 #pragma unroll
-                for (int m = 0; m < GB; ++m) o[(int64_t)m * ld] = v[m];
+                        for (int m = 0; m < GB; ++m) o[(int64_t)m << lg] = v[m];
+                    }
+                } else {
+                    uint32_t *o = out + ((int64_t)kp * BL + (int64_t)g * GB) * ld + pos;
+#pragma unroll
+                    for (int m = 0; m < GB; ++m) o[(int64_t)m * ld] = v[m];
+                }
             }
         }
         __syncthreads();
         if (kp + 2 < kNumPrimes) fetch_tw(kp + 2);
     }
+    if (GAMMA == 0 && prm.slice_mode && prm.p2p) __threadfence_system();  // peer slice stores visible
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1006,7 +1024,7 @@ static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int nti
 
 template <int LOGN2>
 static int launch_rows(const Params &prm, cudaStream_t st, int tile0 = 0, int ntiles = -1) {
-    switch (prm.shard_gamma) {
+    switch (prm.slice_mode ? 0 : prm.shard_gamma) {  // sliced shards run the full slice transform
         case 0: return launch_rows_g<LOGN2, 0>(prm, st, tile0, ntiles);
         case 1: if constexpr (LOGN2 >= 6) return launch_rows_g<LOGN2, 1>(prm, st, tile0, ntiles); break;
         case 2: if constexpr (LOGN2 >= 7) return launch_rows_g<LOGN2, 2>(prm, st, tile0, ntiles); break;
@@ -1073,6 +1091,17 @@ static int launch_cols_mode(const Params &prm, cudaStream_t st) {
         return HK_ECUDA;
     k2_column<LOGN1, TwGlobal, MODE><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
+}
+
+int launch_k2_sliced(const Params &prm, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (prm.log_n1) {
+#define HK_CASE(LG) case LG: return launch_cols_m<LG, 5>(prm, st);
+        HK_CASE(6) HK_CASE(7) HK_CASE(8) HK_CASE(9) HK_CASE(10) HK_CASE(11) HK_CASE(12)
+        HK_CASE(13) HK_CASE(14)
+#undef HK_CASE
+        default: return HK_EUNSUPPORTED;
+    }
 }
 
 int launch_k2_mode(const Params &prm, void *stream, int mode) {

@@ -346,18 +346,30 @@ def main():
         sh = hkdist.CosetShardedMatvec(kind, a, sa, x, sx, P)
         sh.step(check=True)
         ok, why = verify_y(kind, am, asg, xm, xsg, *sh.result(), rank, world, dist, dev)
-        verification = {"fingerprints_all_rows": ok, "p2p_tried": sh.p2p, "detail": why}
-        if not ok and sh.p2p:  # peer-memory exchange gave a wrong y: NCCL exchanges instead
-            sh = hkdist.CosetShardedMatvec(kind, a, sa, x, sx, P, p2p=False)
+        verification = {"fingerprints_all_rows": ok, "p2p_tried": sh.p2p, "sliced_tried": sh.sliced,
+                        "detail": why}
+        # a wrong y (all ranks agree: verify_y all-reduces) falls back one mechanism at a time:
+        # NCCL exchanges instead of peer memory, then the coset (unsliced) forward phase
+        for kw, what in (({"p2p": False}, "NCCL exchanges"), ({"p2p": False, "sliced": False},
+                                                              "NCCL exchanges, unsliced forward")):
+            if ok or (not sh.p2p and not sh.sliced):
+                break
+            if "sliced" not in kw and not sh.p2p:
+                continue
+            sh = hkdist.CosetShardedMatvec(kind, a, sa, x, sx, P, **kw)
             sh.step(check=True)
             ok, why = verify_y(kind, am, asg, xm, xsg, *sh.result(), rank, world, dist, dev)
-            verification.update(fingerprints_all_rows=ok, fallback="NCCL exchanges after a p2p mismatch",
-                                detail=why)
+            verification.update(fingerprints_all_rows=ok, fallback=what + " after a mismatch", detail=why)
         if not ok:
             raise SystemExit(f"bench: sharded y fails its fingerprints ({why})")
         sh_verified_p2p = sh.p2p
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
-        stage_names = ("shard_forward_K1K2", "all_to_all", "shard_finish_K3+all_gather")
+        if sh.sliced:
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+            stage_names = ("shard_slice_K1", "slice_all_to_all", "shard_columns_K2", "all_to_all",
+                           "shard_finish_K3+all_gather")
+        else:
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+            stage_names = ("shard_forward_K1K2", "all_to_all", "shard_finish_K3+all_gather")
 
         def step(i=None):
             if i is None:
@@ -365,14 +377,24 @@ def main():
                 return
             e = ev[i]
             e[0].record(stream)
-            sh.compute_forward()
+            if sh.sliced:
+                sh.compute_slice()
+                e[1].record(stream)
+                sh.exchange_slices()
+                e[2].record(stream)
+                sh.compute_columns()
+                e = e[2:]
+            else:
+                sh.compute_forward()
             e[1].record(stream)
             sh.exchange()
             e[2].record(stream)
             sh.compute_finish()
             sh.gather()
             e[3].record(stream)
-        launches_per_step = 3  # K1 (coset block), K2 (N2/G columns), K3 (row block)
+        # coset: K1 (coset block), K2 (N2/G columns), K3 (row block); sliced: K1 runs as two
+        # launches (this rank's a positions, its x positions)
+        launches_per_step = 4 if sh.sliced else 3
     else:
         from paper_1402_5287_b200 import dist as hkdist
         sh = hkdist.ShardedHankel(a, sa, x, sx, P)
@@ -427,7 +449,7 @@ def main():
         ms_total = float(tt.item())
     ms_step = ms_total / K
     stage_ms = [statistics.mean(ev[i][s].elapsed_time(ev[i][s + 1]) for i in range(K))
-                for s in range(3)]
+                for s in range(len(stage_names))]
     clocks = sampler.summary(wall0, wall1) if sampler else None
     if sampler:
         sampler.stop()
@@ -545,7 +567,8 @@ def main():
     elif args.plan == "coset":
         from paper_1402_5287_b200 import dist as hkdist
         cs = hkdist.CosetStream(kind, (a, sa, x, sx), P, slots=3,
-                                p2p=(getattr(sh, "p2p", False) or "auto") if sh_verified_p2p else False)
+                                p2p=(getattr(sh, "p2p", False) or "auto") if sh_verified_p2p else False,
+                                sliced=sh.sliced)
         probs = [(a, sa, x, sx)] * n_tp
         cs.run(probs[:6])
         torch.cuda.synchronize()
@@ -560,7 +583,8 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         cms = float(tt.item()) / n_tp
         throughput = {"value": 1000.0 / cms, "unit": UNIT, "ms_per_matvec": cms, "matvecs": n_tp,
-                      "in_flight": 3, "p2p": cs.p2p, "launches_per_rank": 3 * n_tp,
+                      "in_flight": 3, "p2p": cs.p2p, "sliced": cs.sliced,
+                      "launches_per_rank": (4 if cs.sliced else 3) * n_tp,
                       "what": "CosetStream: stream of independent matvecs over the sigma-coset shards, 3 slots, "
                               "exchanges on a communication stream overlapping the next matvec's K1/K2; "
                               "CUDA events, max over ranks"}
@@ -811,7 +835,9 @@ def main():
         "config": workload_config(wl),
         "plan": {k: plan[k] for k in ("w", "Ls", "log_n1", "log_n2", "k_primes", "margin_bits")},
         "parallelism": "single GPU" if world == 1 else (
-            (f"sigma-coset x{world}: " + ("exchanges fused into K2/K3 stores over peer memory "
+            (f"sigma-coset x{world}" + (" sliced (each rank slices 1/G of the positions, slice "
+                                         "all-to-all before K2)" if getattr(sh, "sliced", False) else "")
+             + ": " + ("exchanges fused into K1/K2/K3 stores over peer memory "
                                           "(symmetric memory, NVLink) + device barriers"
                                           if getattr(sh, "p2p", False) else
                                           "NCCL all-to-all + all-gather"))

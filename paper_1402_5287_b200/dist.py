@@ -151,16 +151,46 @@ def _cuda_finish(ws, g, recv, y_mag, y_sign):
     shard_finish(ws, g, recv, y_mag, y_sign)
 
 
+def _cuda_slice(ws, g, a_mag, a_sign, x_mag, x_sign, slice_send):
+    from . import shard_slice
+    shard_slice(ws, g, a_mag, a_sign, x_mag, x_sign, slice_send)
+
+
+def _cuda_columns(ws, g, slice_recv, send):
+    from . import shard_columns
+    shard_columns(ws, g, slice_recv, send)
+
+
+def _want_sliced(sliced, info, G) -> bool:
+    """Sliced sharding (each rank slices 1/G of the positions) when the plan supports it: by
+    default from G = 4 on, where the replicated slicing of the coset mode costs more than the
+    extra slice exchange (profiles/r02/shard_phase_times_C3.json); HK_SLICED=0/1 overrides."""
+    ok = int(info.get("slice_buffer_words", 0)) > 0
+    env = os.environ.get("HK_SLICED")
+    if env is not None:
+        return env == "1" and ok
+    if sliced == "auto":
+        return G >= 4 and ok
+    if sliced and not ok:
+        raise ValueError("sliced sharding unsupported for this plan (N1 > 2^14 or too few positions)")
+    return bool(sliced)
+
+
 class CosetShardedMatvec:
     """Prepared sigma-coset-sharded problem (kind in {Hankel, Toeplitz, circulant}, n x n) for
     repeated steps: rank-local workspace, all-to-all send / receive buffers and the padded y.
 
     ``forward(ws, g, a, sa, x, sx, send)`` and ``finish(ws, g, recv, y, s)`` default to the CUDA
     phases (hk_hankel_shard_forward / _finish); tests inject stand-ins to exercise the exchange
-    on CPU (gloo), with ``info`` the layout (paper_1402_5287_b200.shard_plan)."""
+    on CPU (gloo), with ``info`` the layout (paper_1402_5287_b200.shard_plan).
+
+    ``sliced``: the forward phase runs as slice -> slice all-to-all -> columns
+    (hk_hankel_shard_slice / _columns, stand-ins ``slice(ws, g, a, sa, x, sx, slice_send)`` and
+    ``columns(ws, g, slice_recv, send)``): rank g slices and row-transforms only positions
+    [g Rs, (g+1) Rs) of a and x, and gathers its sigma-block from every rank's slices."""
 
     def __init__(self, kind, a_mag, a_sign, x_mag, x_sign, P, group=None, forward=None,
-                 finish=None, info=None, p2p="auto"):
+                 finish=None, info=None, p2p="auto", sliced="auto", slice=None, columns=None):
         import torch
         import torch.distributed as dist
         self.dist, self.group = dist, group
@@ -178,8 +208,15 @@ class CosetShardedMatvec:
         self.info = info
         self.forward = forward or _cuda_forward
         self.finish = finish or _cuda_finish
+        injected = forward is not None or finish is not None
+        self.slice_fn = slice or (None if injected else _cuda_slice)
+        self.columns_fn = columns or (None if injected else _cuda_columns)
+        if self.slice_fn is None or self.columns_fn is None:
+            sliced = False
+        self.sliced = _want_sliced(sliced, info, self.G) if sliced else False
         words, rpr, yr = info["buffer_words"], info["rows_per_rank"], info["y_rows"]
         self.rpr, self.y_rows = int(rpr), int(yr)
+        self.slice_words = int(info.get("slice_buffer_words", 0)) if self.sliced else 0
         Ly = 2 * ((P + 63) // 64) + 1
         self.p2p = False
         if os.environ.get("HK_P2P", "1") == "0":
@@ -195,6 +232,9 @@ class CosetShardedMatvec:
             self.recv = torch.zeros((words,), dtype=torch.int32, device=dev)
             self.y_pad = torch.zeros((yr, Ly), dtype=a_mag.dtype, device=dev)
             self.s_pad = torch.zeros((yr,), dtype=torch.int8, device=dev)
+            if self.sliced:  # zero once: positions no rank owns (past the last entry) stay zero
+                self.slice_send = torch.zeros((self.slice_words,), dtype=torch.int32, device=dev)
+                self.slice_recv = torch.zeros((self.slice_words,), dtype=torch.int32, device=dev)
 
     def _agree(self, ok: bool, dev) -> bool:
         import torch
@@ -208,9 +248,12 @@ class CosetShardedMatvec:
         import torch
         try:
             import torch.distributed._symmetric_memory as symm_mem
-            recv = symm_mem.empty(words, dtype=torch.int32, device=dev)
-            y_pad = symm_mem.empty(yr, Ly, dtype=mag_dtype, device=dev)
-            s_pad = symm_mem.empty(yr, dtype=torch.int8, device=dev)
+            bufs = [symm_mem.empty(words, dtype=torch.int32, device=dev),
+                    symm_mem.empty(yr, Ly, dtype=mag_dtype, device=dev),
+                    symm_mem.empty(yr, dtype=torch.int8, device=dev)]
+            if self.sliced:
+                bufs.append(symm_mem.empty(self.slice_words, dtype=torch.int32, device=dev))
+                bufs[-1].zero_()  # positions no rank owns stay zero (K2 reads them)
             ok = True
         except Exception:
             ok = False
@@ -218,25 +261,54 @@ class CosetShardedMatvec:
             return False
         try:
             grp = self.group if self.group is not None else self.dist.group.WORLD
-            handles = [symm_mem.rendezvous(t, grp) for t in (recv, y_pad, s_pad)]
+            handles = [symm_mem.rendezvous(t, grp) for t in bufs]
 
             def peer_ptrs(t, h):
                 off = t.data_ptr() - int(h.buffer_ptrs[self.rank])
                 return [int(p) + off for p in h.buffer_ptrs]
 
-            ptrs = [peer_ptrs(t, h) for t, h in zip((recv, y_pad, s_pad), handles)]
+            ptrs = [peer_ptrs(t, h) for t, h in zip(bufs, handles)]
             ok = all(len(p) == self.G and all(p) for p in ptrs)
         except Exception:
             ok = False
         if not self._agree(ok, dev):
             return False
-        self.recv, self.y_pad, self.s_pad = recv, y_pad, s_pad
-        self.recv_ptrs, self.y_ptrs, self.s_ptrs = ptrs
+        self.recv, self.y_pad, self.s_pad = bufs[:3]
+        self.recv_ptrs, self.y_ptrs, self.s_ptrs = ptrs[:3]
         self.h_recv, self.h_y = handles[0], handles[1]
+        if self.sliced:
+            self.slice_recv, self.slice_ptrs, self.h_slice = bufs[3], ptrs[3], handles[3]
+            handles[3].barrier()  # every rank's zero-fill is done before any peer stores into it
         return True
 
-    def compute_forward(self):
+    def compute_slice(self):
+        """Sliced phase 1a: K1 over this rank's positions, sigma-blocks scattered by destination."""
         if self.p2p:
+            from . import shard_slice_p2p
+            shard_slice_p2p(self.ws, self.rank, *self.inputs, self.slice_ptrs)
+        else:
+            self.slice_fn(self.ws, self.rank, *self.inputs, self.slice_send)
+
+    def exchange_slices(self):
+        if self.p2p:  # every rank's K1 stores into this rank's slice buffer are done
+            self.h_slice.barrier()
+        else:
+            self.dist.all_to_all_single(self.slice_recv, self.slice_send, group=self.group)
+
+    def compute_columns(self):
+        """Sliced phase 1b: K2 on this rank's sigma-block, gathered from the received slices."""
+        if self.p2p:
+            from . import shard_columns_p2p
+            shard_columns_p2p(self.ws, self.rank, self.slice_recv, self.recv_ptrs)
+        else:
+            self.columns_fn(self.ws, self.rank, self.slice_recv, self.send)
+
+    def compute_forward(self):
+        if self.sliced:
+            self.compute_slice()
+            self.exchange_slices()
+            self.compute_columns()
+        elif self.p2p:
             from . import shard_forward_p2p
             shard_forward_p2p(self.ws, self.rank, *self.inputs, self.recv_ptrs)
         else:
@@ -312,22 +384,35 @@ class CosetStream:
     callback, one more barrier after ``consume`` keeps other ranks' K3 stores of matvec t + S out
     of this rank's y until it has been consumed.
 
+    Sliced slots add a third exchange per matvec: iteration t issues, in this order, the finish of
+    t - 2 (K3, y all-gather), the slicing of t (K1) and its slice all-to-all, then the columns of
+    t - 1 (K2) and its coset all-to-all -- communication order GA(t-2), XS(t), XC(t-1) on every
+    rank, and the compute stream runs K3(t-2), K1(t), K2(t-1) while the exchanges of the
+    neighbouring matvecs are in flight.  The slot-reuse argument above holds unchanged: K1 of
+    matvec t (which with peer memory stores into the peers' slice buffers) waits for the
+    all-gather / barrier of t - S, issued earlier in the same iteration for S = 2.
+
     The CPU (gloo) path runs the same sequence synchronously, for the tests."""
 
     def __init__(self, kind, inputs_like, P, slots=3, group=None, forward=None, finish=None,
-                 info=None, p2p="auto"):
+                 info=None, p2p="auto", sliced="auto", slice=None, columns=None):
         import torch
+        if slots < 2:
+            raise ValueError("CosetStream needs at least 2 slots (slot reuse waits on matvec t - S)")
         self.slots = [CosetShardedMatvec(kind, *inputs_like, P, group=group, forward=forward,
-                                         finish=finish, info=info, p2p=p2p) for _ in range(slots)]
+                                         finish=finish, info=info, p2p=p2p, sliced=sliced,
+                                         slice=slice, columns=columns) for _ in range(slots)]
         self.S = len(self.slots)
         self.cuda = inputs_like[0].is_cuda
         self.p2p = self.slots[0].p2p
+        self.sliced = self.slots[0].sliced
         self.comp = self.comm = None
         if self.cuda:
             self.comp = torch.cuda.current_stream()
             self.comm = torch.cuda.Stream(device=inputs_like[0].device)
             ev = lambda: [torch.cuda.Event() for _ in range(self.S)]  # noqa: E731
             self.ev_fwd, self.ev_x, self.ev_fin, self.ev_done = ev(), ev(), ev(), ev()
+            self.ev_a, self.ev_xs = ev(), ev()
 
     def _stream(self, s):
         import contextlib
@@ -364,7 +449,16 @@ class CosetStream:
                 if self.cuda:
                     self.ev_done[s].record(self.comm)
 
+        def status(sl, prob):
+            if check and sl.ws is not None:
+                w = torch.empty((1,), dtype=torch.int32, device=prob[0].device)
+                w.copy_(sl.ws.status_word())
+                statuses.append(w)
+
         count = 0
+        if self.sliced:
+            count = self._run_sliced(problems, finish, status, used)
+            problems = ()
         for t, prob in enumerate(problems):
             s = t % S
             sl = self.slots[s]
@@ -373,10 +467,7 @@ class CosetStream:
                     self.comp.wait_event(self.ev_done[s])
                 sl.inputs = tuple(prob)
                 sl.compute_forward()
-                if check and sl.ws is not None:
-                    w = torch.empty((1,), dtype=torch.int32, device=prob[0].device)
-                    w.copy_(sl.ws.status_word())
-                    statuses.append(w)
+                status(sl, prob)
                 if self.cuda:
                     self.ev_fwd[s].record(self.comp)
             used[s] = True
@@ -389,7 +480,7 @@ class CosetStream:
             if t >= 1:
                 finish(t - 1)
             count += 1
-        if count:
+        if count and not self.sliced:
             finish(count - 1)
         if self.cuda:
             self.comp.wait_stream(self.comm)
@@ -401,4 +492,54 @@ class CosetStream:
             sl.dist.all_reduce(worst, op=sl.dist.ReduceOp.MIN, group=sl.group)
             if int(worst.item()) != HK_OK:
                 raise HKError(int(worst.item()), "coset stream data status (MIN over ranks)")
+        return count
+
+    def _run_sliced(self, problems, finish, status, used):
+        S = self.S
+
+        def columns(t):
+            s = t % S
+            sl = self.slots[s]
+            with self._stream(self.comp):
+                if self.cuda:
+                    self.comp.wait_event(self.ev_xs[s])
+                sl.compute_columns()
+                if self.cuda:
+                    self.ev_fwd[s].record(self.comp)
+            with self._stream(self.comm):
+                if self.cuda:
+                    self.comm.wait_event(self.ev_fwd[s])
+                sl.exchange()
+                if self.cuda:
+                    self.ev_x[s].record(self.comm)
+
+        count = 0
+        for t, prob in enumerate(problems):
+            s = t % S
+            sl = self.slots[s]
+            if t >= 2:
+                finish(t - 2)
+            with self._stream(self.comp):
+                if self.cuda and used[s]:
+                    self.comp.wait_event(self.ev_done[s])
+                sl.inputs = tuple(prob)
+                sl.compute_slice()
+                status(sl, prob)
+                if self.cuda:
+                    self.ev_a[s].record(self.comp)
+            used[s] = True
+            with self._stream(self.comm):
+                if self.cuda:
+                    self.comm.wait_event(self.ev_a[s])
+                sl.exchange_slices()
+                if self.cuda:
+                    self.ev_xs[s].record(self.comm)
+            if t >= 1:
+                columns(t - 1)
+            count += 1
+        if count:
+            columns(count - 1)
+            if count >= 2:
+                finish(count - 2)
+            finish(count - 1)
         return count

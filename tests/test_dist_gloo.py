@@ -161,7 +161,7 @@ def test_coset_exchange_gloo_world2(kind, n, P):
 # throughput mode (CosetStream): a stream of independent matvecs over S slots.  Stand-in phases
 # tag every word with the problem id, so the test pins that each consumed y holds the blocks of
 # its own problem from every rank, in order, across slot reuse.
-def _stream_worker(rank, world, port, kind, n, P, nprob, slots, q):
+def _stream_worker(rank, world, port, kind, n, P, nprob, slots, q, sliced=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -197,21 +197,44 @@ def _stream_worker(rank, world, port, kind, n, P, nprob, slots, q):
             got.append((t, [int(ym[0, 0]), int(ym[-1, 0])],
                         sorted({int(v) for v in sh.slots[t % slots].y_pad[:, 0]})))
 
-        sh = hd.CosetStream(kind, base, P, slots=slots, forward=forward, finish=finish, info=info)
+        kw = {}
+        if sliced:  # slice stand-in tags (problem, source, destination); columns checks the routing
+            sc = info["slice_chunk_words"]
+
+            def slice_(ws, g, am, asg, xm, xsg, slice_send):
+                pid = int(am[0, 0])
+                for dst in range(world):
+                    slice_send[dst * sc:(dst + 1) * sc] = pid * 100 + g * 10 + dst
+
+            def columns(ws, g, slice_recv, send):
+                pids = {int(slice_recv[src * sc]) // 100 for src in range(world)}
+                assert len(pids) == 1, pids
+                routed = [int(slice_recv[src * sc]) % 100 for src in range(world)]
+                assert routed == [src * 10 + g for src in range(world)], routed
+                pid = pids.pop()
+                for dst in range(world):
+                    send[dst * chunk:(dst + 1) * chunk] = pid * 100 + g * 10 + dst
+
+            kw = dict(sliced=True, slice=slice_, columns=columns)
+        sh = hd.CosetStream(kind, base, P, slots=slots, forward=forward, finish=finish, info=info, **kw)
+        assert sh.sliced == sliced
         cnt = sh.run(probs, consume=consume)
         q.put((rank, cnt, got, rpr, info["y_rows"]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,slots", [(0, 3), (1, 2), (2, 3)])
-def test_coset_stream_gloo_world2(kind, slots):
-    import paper_1402_5287_b200 as hk
+@pytest.mark.parametrize("kind,slots,sliced", [(0, 3, False), (1, 2, False), (2, 3, False),
+                                               (0, 2, True), (1, 3, True), (2, 2, True)])
+def test_coset_stream_gloo_world2(kind, slots, sliced):
+    """Sliced: the slice all-to-all, the coset all-to-all and the y all-gather of 7 problems
+    interleave over 2-3 slots; every phase sees only its own problem's words, correctly routed."""
     world, n, P, nprob = 2, 64, 4200, 7
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_stream_worker, args=(r, world, port, kind, n, P, nprob, slots, q))
+    procs = [ctx.Process(target=_stream_worker,
+                         args=(r, world, port, kind, n, P, nprob, slots, q, sliced))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -280,3 +303,20 @@ def test_p2p_setup_falls_back_together(fail_rank):
         assert p.exitcode == 0
     for rank, ok, rendezvous_calls in res:
         assert ok is False and rendezvous_calls == 0
+
+
+def test_sliced_mode_selection(monkeypatch):
+    """Auto: sliced from G = 4 on when the plan supports it; HK_SLICED=0/1 overrides; an explicit
+    request the plan cannot serve raises."""
+    from paper_1402_5287_b200.dist import _want_sliced
+    ok, no = {"slice_buffer_words": 10}, {"slice_buffer_words": 0}
+    monkeypatch.delenv("HK_SLICED", raising=False)
+    assert [_want_sliced("auto", ok, G) for G in (2, 4, 8)] == [False, True, True]
+    assert _want_sliced("auto", no, 8) is False
+    assert _want_sliced(True, ok, 2) is True
+    with pytest.raises(ValueError):
+        _want_sliced(True, no, 4)
+    monkeypatch.setenv("HK_SLICED", "0")
+    assert _want_sliced("auto", ok, 8) is False
+    monkeypatch.setenv("HK_SLICED", "1")
+    assert _want_sliced("auto", ok, 2) is True and _want_sliced("auto", no, 2) is False

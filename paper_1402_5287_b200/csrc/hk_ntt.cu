@@ -106,8 +106,10 @@ constexpr int k1_threads() {
 // "difference x twiddle" (bit 1) half selected by b's bits from the top -- i.e. the coset fold.
 // Block b holds the transform outputs at bit-reversed positions [b N2 / G, (b + 1) N2 / G), the
 // frequencies congruent to bitrev(b) mod G.
-template <int LOGN2, int GAMMA>
+template <int LOGN2, int GSEL>  // GSEL = gamma (coset shards keep N2 / 2^gamma outputs), -1: sliced shards
 __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rowntt(Params prm, int tiles_a) {
+    constexpr int GAMMA = GSEL < 0 ? 0 : GSEL;
+    constexpr bool SLICED = GSEL < 0;
     constexpr int N2 = 1 << LOGN2;
     constexpr int BL = N2 >> GAMMA;          // outputs kept per row and prime
     constexpr int GK = 32 >> GAMMA;          // top-pass points kept per group
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
             const int64_t orow = r0 + rr;
             if (orow < count) {
                 const int64_t pos = rev ? (count - 1 - orow) : orow;
-                if (GAMMA == 0 && prm.slice_mode) {
+                if constexpr (SLICED) {
                     // sliced shards: positions [src Rs, (src+1) Rs) of this rank only; sigma-block
                     // d = (g GB) / n2loc goes to chunk d of the send buffer (or, over peer memory,
                     // to chunk src of rank d's receive buffer)
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         __syncthreads();
         if (kp + 2 < kNumPrimes) fetch_tw(kp + 2);
     }
-    if (GAMMA == 0 && prm.slice_mode && prm.p2p) __threadfence_system();  // peer slice stores visible
+    if constexpr (SLICED) if (prm.p2p) __threadfence_system();  // peer slice stores visible
 }
 
 // ------------------------------------------------------------------------------------------
@@ -377,6 +379,13 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
 #endif
 #ifndef HK_K3_MINB
 #define HK_K3_MINB 2
+#endif
+#ifndef HK_K3_GARNER_X2
+#define HK_K3_GARNER_X2 0  // two Garner slots per thread per round
+#endif
+#ifndef HK_K3_SKIP
+#define HK_K3_SKIP 0  // dev timing only (wrong results): 1 skips the inverse NTTs, 2 Garner, 4 the
+                      // gather, 8 the Y^ load, 16 the y store
 #endif
 template <int LOGN2>
 constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : HK_K3_ROWS; }
@@ -602,6 +611,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t r0 = prm.row0 + (int64_t)blockIdx.x * R;
     const int64_t m = prm.m;
+    if (HK_K3_SKIP & 32) return;
     const int64_t vb = (int64_t)blockIdx.y;  // batch vector (0 unless hk_matvec_prepared_batch)
     const uint32_t *Yhat = prm.Yhat + vb * (int64_t)kNumPrimes * N2 * prm.ldY;
     uint64_t *y_mag = prm.y_mag + vb * prm.y_vstride * (prm.round_out ? prm.L + 1 : prm.Ly);
@@ -621,7 +631,9 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
                     (r0 - prm.shard_row0);
             }
             uint32_t *d = sm + LY::idx(kp, sg, 0);
-            if (vec) {
+            if (HK_K3_SKIP & 8) {
+                d[0] = e;
+            } else if (vec) {
                 if constexpr (R == 8) { cp_async16(d, g); cp_async16(d + 4, g + 4); }
                 else if constexpr (R == 4) cp_async16(d, g);
                 else cp_async8(d, g);
@@ -634,8 +646,39 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
         __syncthreads();
     }
     // (a) inverse slice NTTs
+#if !(HK_K3_SKIP & 1)
     K3Dit<LOGN2, 0>::run(sm, prm);
-#if HK_K3_GARNER_SLOT
+#endif
+#if HK_K3_SKIP & 2
+#elif HK_K3_GARNER_X2 && HK_K3_V2
+    // (b) Garner CRT in place, two slots per thread per round (independent chains interleave)
+    for (int it = tid; it < R * N2; it += 2 * T) {
+        const int itb = it + T < R * N2 ? it + T : it;
+        const int r = it % R, sg = it / R, rb = itb % R, sgb = itb / R;
+        uint32_t ra[kNumPrimes], rbv[kNumPrimes], ca[kNumPrimes], cb[kNumPrimes];
+#pragma unroll
+        for (int kp = 0; kp < kNumPrimes; ++kp) {
+            ra[kp] = sm[LY::idx(kp, sg, r)];
+            rbv[kp] = sm[LY::idx(kp, sgb, rb)];
+        }
+        garner2(ra, prm, ca);
+        garner2(rbv, prm, cb);
+        if (sg == 1) {
+#pragma unroll
+            for (int k = 0; k < kNumPrimes; ++k) ca[k] = 0;
+        }
+        if (sgb == 1) {
+#pragma unroll
+            for (int k = 0; k < kNumPrimes; ++k) cb[k] = 0;
+        }
+#pragma unroll
+        for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, sg, r)] = ca[k];
+        if (itb != it) {
+#pragma unroll
+            for (int k = 0; k < kNumPrimes; ++k) sm[LY::idx(k, sgb, rb)] = cb[k];
+        }
+    }
+#elif HK_K3_GARNER_SLOT
     // (b) Garner CRT in place, slot by slot: coefficient s lives at sigma = (N2 - s) mod N2 and its
     // CRT words overwrite its own residues there, so any thread may take any slot (R N2 slots over
     // the block: no pairing, no remainder round of pairs)
@@ -705,8 +748,15 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     int e_prev = 0;
     uint32_t gbits = 0, pbits = 0;
     uint32_t Gt = 0, Pt = 1;         // (G, P) of limbs 1 .. c
+#if HK_K3_SKIP & 4
+#pragma unroll
+    for (int c = 0; c < CH; ++c) u[c] = smr[c * R];
+#pragma unroll
+    for (int j = 0; j < 0; ++j) {
+#else
 #pragma unroll
     for (int j = 0; j < CH + 3; ++j) {
+#endif
         const uint32_t qm = __ldg(qmap + j);
         const uint32_t o = qm >> 6, sh = qm & 63u;
         const uint32_t w0 = smr[o], w1 = smr[LY::PS + o], w2 = smr[2 * LY::PS + o],
@@ -926,7 +976,9 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     }
     __syncthreads();
 #if HK_K3_FLAT_STORE
-    if (!prm.round_out) {
+    if (HK_K3_SKIP & 16) {
+        if (tid < R && ybuf[tid] == 12345) y_mag[tid] = 1;
+    } else if (!prm.round_out) {
         // the R rows' limbs as one flat range (R Ly / T rounds instead of R ceil(Ly / T)); (rr, l)
         // advance incrementally (no division; T may exceed Ly for small P)
         const int nr = (int)(m - r0 < R ? m - r0 : R);
@@ -1024,7 +1076,8 @@ static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int nti
 
 template <int LOGN2>
 static int launch_rows(const Params &prm, cudaStream_t st, int tile0 = 0, int ntiles = -1) {
-    switch (prm.slice_mode ? 0 : prm.shard_gamma) {  // sliced shards run the full slice transform
+    if (prm.slice_mode) return launch_rows_g<LOGN2, -1>(prm, st, tile0, ntiles);  // full slice transform
+    switch (prm.shard_gamma) {
         case 0: return launch_rows_g<LOGN2, 0>(prm, st, tile0, ntiles);
         case 1: if constexpr (LOGN2 >= 6) return launch_rows_g<LOGN2, 1>(prm, st, tile0, ntiles); break;
         case 2: if constexpr (LOGN2 >= 7) return launch_rows_g<LOGN2, 2>(prm, st, tile0, ntiles); break;

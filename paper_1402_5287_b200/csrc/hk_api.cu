@@ -866,21 +866,24 @@ static int launch_slice_k1(const Plan &pl, const Params &prm, int32_t g, void *s
     const int kT = k1_tile_rows();
     const int ga = k1_tiles_a(prm), gx = k1_tiles_x(prm);
     const int64_t na = pl.info.a_count, n = pl.info.n;
+    int a0 = 0, a1 = 0, x0 = 0, x1 = 0;  // tile ranges (x: combined index ga + t)
     int64_t lo = (int64_t)g * pl.rs_a, hi = lo + pl.rs_a < na ? lo + pl.rs_a : na;
-    int rc;
-    if (hi > lo) {
-        const int t0 = (int)(lo / kT), t1 = (int)((hi + kT - 1) / kT);
-        if ((rc = launch_k1_range(prm, stream, t0, t1 - t0))) return rc;
-    }
+    if (hi > lo) a0 = (int)(lo / kT), a1 = (int)((hi + kT - 1) / kT);
     lo = (int64_t)g * pl.rs_x;
     hi = lo + pl.rs_x < n ? lo + pl.rs_x : n;
     if (hi > lo) {
         const int64_t r_lo = pl.x_reversed ? n - hi : lo, r_hi = pl.x_reversed ? n - lo : hi;
-        const int t0 = (int)(r_lo / kT), t1 = (int)((r_hi + kT - 1) / kT);
-        if ((rc = launch_k1_range(prm, stream, ga + t0, t1 - t0))) return rc;
+        x0 = ga + (int)(r_lo / kT), x1 = ga + (int)((r_hi + kT - 1) / kT);
     }
     (void)gx;
-    return HK_OK;
+    if (a1 == a0 && x1 == x0) return HK_OK;
+    if (a1 == a0) return launch_k1_range(prm, stream, x0, x1 - x0);
+    if (x1 == x0) return launch_k1_range(prm, stream, a0, a1 - a0);
+    // both ranges in one launch (each alone is well under one wave at G >= 4)
+    Params p2 = prm;
+    p2.tile_split = a1 - a0;
+    p2.tile_skip = x0 - a1;
+    return launch_k1_range(p2, stream, a0, (a1 - a0) + (x1 - x0));
 }
 
 int32_t hk_hankel_shard_slice(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,

@@ -100,18 +100,27 @@ HK_DEV void k2_dif_top_from_global(const uint32_t *__restrict__ src, bool zu, ui
 
 // Sliced shards: the same top pass with the column gathered from the slice receive buffer, where
 // matrix position i of this column sits in source (i >> lg)'s chunk at offset i & (2^lg - 1).
-template <class TW, int LOGN, int T, bool ZU>
-HK_DEV void k2_dif_top_gather(const uint32_t *__restrict__ src, size_t chunk, int lg, uint32_t *sm,
-                              const uint2 *tw, uint32_t p) {
+// Point m of group j0 is position j0 + m S.  When 2^lg >= S (Q = lg - log2 S >= 0) a group never
+// crosses a segment boundary: point m lies in segment m >> Q at offset (m mod 2^Q) S + j0, so with Q
+// a template parameter each segment is one base pointer and the loads take immediate offsets.
+template <class TW, int LOGN, int T, bool ZU, int Q>
+HK_DEV void k2_dif_top_gather_q(const uint32_t *__restrict__ src, size_t chunk, int lg, uint32_t *sm,
+                                const uint2 *tw, uint32_t p) {
     constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
     const unsigned mask = (1u << lg) - 1u;
     for (int j0 = threadIdx.x; j0 < S; j0 += T) {
         uint32_t v[G];
 #pragma unroll
         for (int m = 0; m < G; ++m) {
-            const unsigned i = (unsigned)(j0 + m * S);
-            if (ZU && m >= G / 2) v[m] = 0u;
-            else v[m] = __ldcs(src + (size_t)(i >> lg) * chunk + (i & mask));
+            if (ZU && m >= G / 2) {
+                v[m] = 0u;
+            } else if constexpr (Q >= 0) {
+                const uint32_t *seg = src + (size_t)(m >> Q) * chunk + j0;
+                v[m] = __ldcs(seg + (m & ((1 << Q) - 1)) * S);
+            } else {
+                const unsigned i = (unsigned)(j0 + m * S);
+                v[m] = __ldcs(src + (size_t)(i >> lg) * chunk + (i & mask));
+            }
         }
 #pragma unroll
         for (int l = R - 1; l >= 0; --l) {
@@ -133,6 +142,18 @@ HK_DEV void k2_dif_top_gather(const uint32_t *__restrict__ src, size_t chunk, in
         for (int m = 0; m < G; ++m) b0[padded_len(m * S)] = v[m];
     }
     __syncthreads();
+}
+template <class TW, int LOGN, int T, bool ZU>
+HK_DEV void k2_dif_top_gather(const uint32_t *__restrict__ src, size_t chunk, int lg, uint32_t *sm,
+                              const uint2 *tw, uint32_t p) {
+    switch (lg - (LOGN - 5)) {
+        case 0: k2_dif_top_gather_q<TW, LOGN, T, ZU, 0>(src, chunk, lg, sm, tw, p); break;
+        case 1: k2_dif_top_gather_q<TW, LOGN, T, ZU, 1>(src, chunk, lg, sm, tw, p); break;
+        case 2: k2_dif_top_gather_q<TW, LOGN, T, ZU, 2>(src, chunk, lg, sm, tw, p); break;
+        case 3: k2_dif_top_gather_q<TW, LOGN, T, ZU, 3>(src, chunk, lg, sm, tw, p); break;
+        case 4: k2_dif_top_gather_q<TW, LOGN, T, ZU, 4>(src, chunk, lg, sm, tw, p); break;
+        default: k2_dif_top_gather_q<TW, LOGN, T, ZU, -1>(src, chunk, lg, sm, tw, p); break;
+    }
 }
 
 // Middle forward passes (R = 5), k = 1 .. NP-2.
@@ -280,6 +301,18 @@ HK_DEV void k2_column_body(const Params &prm, uint32_t *sm, const uint2 *twf, in
             const uint32_t *g = prm.Ahat + cidx * prm.ldA;
             for (int c = tid; c < nch; c += T) cp_async16(sA + 4 * c, g + 4 * c);
         }
+    } else if (HK_K2_L2PF && SLICED) {
+        // the A^ column's G segments (one per source rank) into L2 during X^'s transform, and the
+        // X^ segments of the column about one wave ahead
+        const int G = 1 << prm.shard_gamma;
+        if (tid < G)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(slA + (size_t)tid * prm.slice_chunk),
+                         "r"(4u << prm.lg_rs_a) : "memory");
+        const size_t nxt = cidx + HK_K2_L2PF_NEXT;
+        if (HK_K2_L2PF_NEXT && tid >= 32 && tid < 32 + G && nxt < (size_t)kNumPrimes * prm.n2loc)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n"
+                         ::"l"(prm.slice_in + prm.slice_xoff + (nxt << prm.lg_rs_x) + (size_t)(tid - 32) * prm.slice_chunk),
+                         "r"(4u << prm.lg_rs_x) : "memory");
     } else if (HK_K2_L2PF && !SLICED && tid == 0) {
         // no staging room: have the A^ column brought into L2 (bulk prefetch) during X^'s transform
         const uint32_t *g = prm.Ahat + cidx * prm.ldA;

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         if (tid == 0 && blockIdx.x == 0) atomicMin(&prm.hdr->status, (int)HK_EINVAL);
         return;
     }
-    const int bt = (int)blockIdx.x + prm.tile0;
+    const int bt = (int)blockIdx.x + prm.tile0 + ((int)blockIdx.x >= prm.tile_split ? prm.tile_skip : 0);
     const bool is_x = bt >= tiles_a;
     if (prm.need_a_ready && prm.hdr->a_ready != 1) {
         if (tid == 0) atomicMin(&prm.hdr->status, (int)HK_EINVAL);

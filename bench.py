@@ -104,6 +104,42 @@ def workload(cfg_name):
                      f"{c['recipe']}")
 
 
+def pcie_roofline(h2d, d2h, ms_e2e, dev):
+    """The e2e step's own roofline: pinned-copy bandwidth of this box measured here (64 MiB copies,
+    CUDA events; H2D and D2H concurrently on two streams, as the pipeline runs them), and the
+    fraction of the e2e step those bytes need at that rate."""
+    import torch
+    nb = 64 << 20
+    hs = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    ds = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def both():
+        with torch.cuda.stream(s1):
+            ds[0].copy_(hs[0], non_blocking=True)
+        with torch.cuda.stream(s2):
+            hs[1].copy_(ds[1], non_blocking=True)
+
+    def one(up):
+        with torch.cuda.stream(s1):
+            (ds[0].copy_(hs[0], non_blocking=True) if up else hs[1].copy_(ds[1], non_blocking=True))
+
+    res = {}
+    for name, fn in (("h2d", lambda: one(True)), ("d2h", lambda: one(False)), ("both", both)):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(5):
+            fn()
+        torch.cuda.synchronize()
+        res[name] = (2 if name == "both" else 1) * 5 * nb / (time.perf_counter() - t0) / 1e9
+    t_copy = max(h2d / (res["h2d"] * 1e9), d2h / (res["d2h"] * 1e9), (h2d + d2h) / (res["both"] * 1e9))
+    return {"h2d_gbs": res["h2d"], "d2h_gbs": res["d2h"], "bidir_gbs": res["both"],
+            "t_copy_ms": t_copy * 1e3, "frac": t_copy * 1e3 / ms_e2e,
+            "what": "pinned host<->device bandwidth measured in this run (64 MiB copies, wall clock); "
+                    "t_copy = max(h2d / H2D, d2h / D2H, (h2d + d2h) / bidirectional); frac = t_copy / e2e step"}
+
+
 def workload_config(wl):
     """The `config` object, identical for both arms (the workload, and the L2 note the contract asks for)."""
     return {"workload": wl["desc"], "kind": gen.KIND_NAMES[wl["kind"]], "n": wl["n"], "P": wl["P"],
@@ -700,7 +736,8 @@ def main():
                       "buffers; lanes overlap one call's copies with another's kernels)",
                "timing": "host wall clock from first submit to drain (all device work complete)",
                "latency_ms_single_call": ms_lat,
-               "single_call_api": "hk_matvec_host (synchronous)"}
+               "single_call_api": "hk_matvec_host (synchronous)",
+               "pcie": pcie_roofline(h2d, d2h, ms_e2e, dev)}
         del pipe
 
     # ---- e2e at N > 1: every step each rank copies its (replicated) a and x from pinned host memory,

@@ -282,7 +282,8 @@ def test_config_sampled(hk, name):
 
 # ---------------------------------------------------------------------------------------------
 # companion A6: schoolbook kernel
-@pytest.mark.parametrize("n,P", [(1, 64), (5, 65), (64, 3328), (100, 1000), (33, 16608)])
+@pytest.mark.parametrize("n,P", [(1, 64), (1, 1), (2, 32), (5, 65), (7, 33), (64, 3328), (100, 1000),
+                                 (33, 16608), (300, 200), (257, 3328), (5, 40000), (3, 33216)])
 def test_schoolbook_parity(hk, n, P):
     for kind in (0, 1, 2):
         am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=n + 7)
@@ -292,6 +293,46 @@ def test_schoolbook_parity(hk, n, P):
         torch.cuda.synchronize()
         assert_same(hk.to_host(ym, ys), oracle.matvec(kind, P, am, asg, xm, xsg),
                     f"schoolbook kind={kind} n={n} P={P}")
+
+
+def test_schoolbook_carry_stress_and_rect(hk):
+    """Carry-stress mantissas (long runs of ones / zeros, signs mixed) for all kinds, and the
+    rectangular Hankel window (m < n rows) that the row-block plan uses."""
+    for kind, n, P in ((0, 96, 3328), (1, 64, 1000), (2, 48, 16608)):
+        am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=3, recipe="carry_stress")
+        a, sa = hk.to_device(am, asg)
+        x, sx = hk.to_device(xm, xsg)
+        ym, ys = hk.schoolbook_matvec(kind, a, sa, x, sx, P)
+        torch.cuda.synchronize()
+        assert_same(hk.to_host(ym, ys), oracle.matvec(kind, P, am, asg, xm, xsg), f"stress {kind}")
+    n, m, P = 40, 9, 2000
+    am, asg, xm, xsg = gen.make_inputs(0, n, P, seed=5)
+    am, asg = am[: m + n - 1], asg[: m + n - 1]
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    ym, ys = hk.schoolbook_matvec(0, a, sa, x, sx, P, m=m)
+    torch.cuda.synchronize()
+    want = oracle.matvec(0, P, am, asg, xm, xsg, m=m)
+    assert_same(hk.to_host(ym, ys), want, "rect")
+
+
+def test_schoolbook_max_magnitude(hk):
+    """Closed form: every entry +(2^P - 1) gives y_i = n (2^P - 1)^2 (the largest output)."""
+    n, P = 37, 1000
+    L = (P + 63) // 64
+    full = np.zeros(L, dtype=np.uint64)
+    for l in range(L):
+        bits = min(64, P - 64 * l)
+        full[l] = np.uint64((1 << bits) - 1)
+    am = np.tile(full, (2 * n - 1, 1)); asg = np.ones(2 * n - 1, dtype=np.int8)
+    xm = np.tile(full, (n, 1)); xsg = np.ones(n, dtype=np.int8)
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    ym, ys = hk.to_host(*hk.schoolbook_matvec(0, a, sa, x, sx, P))
+    want = n * ((1 << P) - 1) ** 2
+    for i in range(n):
+        got = sum(int(ym[i, l]) << (64 * l) for l in range(ym.shape[1]))
+        assert got == want and ys[i] == 1
 
 
 # ---------------------------------------------------------------------------------------------

@@ -90,6 +90,8 @@ def parse():
     ap.add_argument("--config", default="C3", choices=sorted(gen.CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N = 1: launch every timed step from the host instead of replaying its CUDA graph")
     ap.add_argument("--plan", default="coset", choices=["coset", "rowblock"],
                     help="multi-GPU plan (N > 1): SURVEY 8(e) P-2 sigma-coset (default) or P-3 row blocks")
     return ap.parse_args()
@@ -362,9 +364,12 @@ def main():
             raise SystemExit(f"bench: y fails its fingerprints ({why})")
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
 
+        if not args.no_graph:  # whole steps replayed from a CUDA graph (one host call per step)
+            prob.capture()
+
         def step(i=None):
             if i is None:
-                prob.run()
+                prob.run() if args.no_graph else prob.replay()
                 return
             e = ev[i]
             e[0].record(stream)
@@ -887,6 +892,8 @@ def main():
                                           if getattr(sh, "p2p", False) else
                                           "NCCL all-to-all + all-gather"))
             if args.plan == "coset" else f"row-block x{world} + NCCL all-gather"),
+        "launch": ("host call per step" if (world > 1 or args.no_graph) else
+                   "CUDA graph replay per step (Problem.capture: the same K1/K2/K3 launches)"),
         "stages_ms": dict(zip(stage_names, stage_ms)),
         "roofline": roof,
         "verification": verification,

@@ -79,7 +79,7 @@ Big big_pow2_minus1(int w) {  // 2^w - 1
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Plan *pl, int32_t G = 1) {
+int make_plan_uncached(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Plan *pl, int32_t G) {
     if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || m < 1 || P < 1) return HK_EINVAL;
     if (kind != HK_HANKEL && m != n) return HK_EINVAL;
     std::memset(pl, 0, sizeof(*pl));
@@ -205,6 +205,44 @@ int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Pla
     if ((flags & HK_WS_STAGING) && (flags & HK_WS_PREPARED)) return HK_EINVAL;
     if (flags & ~(HK_WS_STAGING | HK_WS_PREPARED)) return HK_EINVAL;
     return HK_OK;
+}
+
+// Plans are pure functions of (kind, m, n, P, flags, G): the last 16 are kept, so a repeated call
+// skips the capacity search (big-integer bounds) on the host.
+int make_plan(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags, Plan *pl, int32_t G = 1) {
+    struct Key {
+        int32_t kind;
+        int64_t m, n;
+        int32_t P;
+        uint32_t flags;
+        int32_t G;
+        bool operator==(const Key &o) const {
+            return kind == o.kind && m == o.m && n == o.n && P == o.P && flags == o.flags && G == o.G;
+        }
+    };
+    constexpr int kCache = 16;
+    static std::mutex mu;
+    static Key keys[kCache];
+    static Plan plans[kCache];
+    static int rcs[kCache];
+    static int used = 0, next = 0;
+    const Key key{kind, m, n, P, flags, G};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (int k = 0; k < used; ++k)
+            if (keys[k] == key) {
+                *pl = plans[k];
+                return rcs[k];
+            }
+    }
+    const int rc = make_plan_uncached(kind, m, n, P, flags, pl, G);
+    std::lock_guard<std::mutex> lk(mu);
+    keys[next] = key;
+    plans[next] = *pl;
+    rcs[next] = rc;
+    next = (next + 1) % kCache;
+    if (used < kCache) ++used;
+    return rc;
 }
 
 uint64_t plan_hash(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t G = 1) {

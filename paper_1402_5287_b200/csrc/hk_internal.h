@@ -70,6 +70,7 @@ struct Params {
     uint64_t hash;
     int32_t tile0;               // K1: first tile of this launch (combined [a tiles | x tiles] index)
     int32_t tile_split, tile_skip;  // K1: CTAs >= tile_split skip tile_skip tiles (two ranges, one launch)
+    int32_t k1_prime_split;      // K1: one prime per CTA (blockIdx.z) for launches under one wave
     int64_t row0;                // K3: first output row of this launch
     // sigma-coset sharding (SURVEY.md 8(e) plan P-2; 1 shard = the single-GPU path):
     int32_t n2loc, log_n2loc;    // transform-domain columns per prime held here (N2 / G)

@@ -10,6 +10,9 @@
 //                        A4 carry propagation and sign-magnitude output (one launch, rows tiled)
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <unordered_map>
+
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +22,21 @@
 #include "hk_k2.cuh"
 
 namespace hk {
+
+// Raise a kernel's dynamic shared-memory limit once per (kernel, size) instead of on every launch
+// (the attribute call is host time that small problems feel; one device per process).
+static int ensure_smem(const void *kern, size_t smem) {
+    if (smem <= 48 * 1024) return HK_OK;
+    static std::mutex mu;
+    static std::unordered_map<const void *, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &cur = done[kern];
+    if (smem <= cur) return HK_OK;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return HK_ECUDA;
+    cur = smem;
+    return HK_OK;
+}
 
 // ------------------------------------------------------------------------------------------
 // K0: twiddle tables.  Per prime: [N2 table | N1 table]; entry h + j of a table of length N
@@ -240,14 +258,17 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
         cp_async_commit();
     };
     __syncthreads();  // every thread is done with the limbs
-    fetch_tw(0);
-    fetch_tw(1);
-    for (int kp = 0; kp < kNumPrimes; ++kp) {
+    // primes [kb, ke): all five, or (launches under one wave, prm.k1_prime_split) blockIdx.z's
+    const int kb = prm.k1_prime_split ? (int)blockIdx.z : 0;
+    const int ke = prm.k1_prime_split ? kb + 1 : kNumPrimes;
+    fetch_tw(kb);
+    if (kb + 1 < ke) fetch_tw(kb + 1);
+    for (int kp = kb; kp < ke; ++kp) {
         const uint32_t p = prm.pc[kp].p;
         const uint32_t *F = is_x ? prm.pc[kp].fx : prm.pc[kp].fa;
         const uint32_t *Fq = is_x ? prm.pc[kp].fx_q : prm.pc[kp].fa_q;
         const uint2 *tw = stw + (kp & 1) * N2;
-        if (kp + 1 < kNumPrimes) cp_async_wait_group<1>();
+        if (kp + 1 < ke) cp_async_wait_group<1>();
         else cp_async_wait_group<0>();
         __syncthreads();
         if (act) {
@@ -347,7 +368,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
             }
         }
         __syncthreads();
-        if (kp + 2 < kNumPrimes) fetch_tw(kp + 2);
+        if (kp + 2 < ke) fetch_tw(kp + 2);
     }
     if constexpr (SLICED) if (prm.p2p) __threadfence_system();  // peer slice stores visible
 }
@@ -1067,10 +1088,21 @@ static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int nti
     prm.tile0 = tile0;
     const size_t tab_bytes = (size_t)2 * (1 << LOGN2) * sizeof(uint2);  // 2 twiddle tables
     const size_t smem1 = (size_t)k1_transform_words(k1_row_stride<LOGN2>(), prm.L) * sizeof(uint32_t) + tab_bytes;
-    if (cudaFuncSetAttribute(k1_slice_rowntt<LOGN2, GAMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem1) != cudaSuccess)
-        return HK_ECUDA;
-    k1_slice_rowntt<LOGN2, GAMMA><<<dim3((unsigned)ntiles, (unsigned)prm.nvec), k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
+    if (ensure_smem((const void *)k1_slice_rowntt<LOGN2, GAMMA>, smem1)) return HK_ECUDA;
+    // a launch under one wave (3 CTAs per SM) runs one prime per CTA: 5x the CTAs, each slicing
+    // its tile again (C1: 24 tiles -> 120 CTAs)
+    static int nsm = 0;
+    if (nsm == 0) {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+            nsm = v;
+        else
+            return HK_ECUDA;
+    }
+    prm.k1_prime_split = (int64_t)ntiles * prm.nvec * kNumPrimes <= (int64_t)HK_K1_MINB * nsm ? 1 : 0;
+    k1_slice_rowntt<LOGN2, GAMMA><<<dim3((unsigned)ntiles, (unsigned)prm.nvec, prm.k1_prime_split ? kNumPrimes : 1),
+                                     k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();
 }
 
@@ -1090,9 +1122,7 @@ template <int LOGN1, int MODE>
 static int launch_cols_m(const Params &prm, cudaStream_t st) {
     const int ncols = kNumPrimes * prm.n2loc;
     const size_t smem = k2_smem_bytes<LOGN1>();
-    if (cudaFuncSetAttribute(k2_column<LOGN1, TwGlobal, MODE>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return HK_ECUDA;
+    if (ensure_smem((const void *)k2_column<LOGN1, TwGlobal, MODE>, smem)) return HK_ECUDA;
     k2_column<LOGN1, TwGlobal, MODE><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
 }
@@ -1139,9 +1169,7 @@ template <int LOGN1, int MODE>
 static int launch_cols_mode(const Params &prm, cudaStream_t st) {
     const int ncols = kNumPrimes * prm.n2loc * (MODE == 2 ? prm.nvec : 1);
     const size_t smem = (size_t)padded_len(1 << LOGN1) * sizeof(uint32_t);
-    if (cudaFuncSetAttribute(k2_column<LOGN1, TwGlobal, MODE>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return HK_ECUDA;
+    if (ensure_smem((const void *)k2_column<LOGN1, TwGlobal, MODE>, smem)) return HK_ECUDA;
     k2_column<LOGN1, TwGlobal, MODE><<<ncols, k2_threads<LOGN1>(), smem, st>>>(prm);
     return check_launch();
 }
@@ -1199,9 +1227,7 @@ static int launch_k3(const Params &prm, cudaStream_t st, int64_t nrows) {
     const size_t ybytes = (size_t)k3_rows<LOGN2>() * prm.Ly * sizeof(uint64_t);  // y rows reuse the area
     const size_t rbytes = K3Layout<LOGN2>::res_words() * sizeof(uint32_t);
     const size_t smem = rbytes > ybytes ? rbytes : ybytes;
-    if (cudaFuncSetAttribute(k3_finish<LOGN2, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return HK_ECUDA;
+    if (ensure_smem((const void *)k3_finish<LOGN2, CH>, smem)) return HK_ECUDA;
     const unsigned grid = (unsigned)((nrows + k3_rows<LOGN2>() - 1) / k3_rows<LOGN2>());
     k3_finish<LOGN2, CH><<<dim3(grid, (unsigned)prm.nvec), k3_threads<LOGN2>(), smem, st>>>(prm);
     return check_launch();

@@ -66,3 +66,15 @@ def test_config_matches_oracle_digest(hk, name):
         got = row_digests(ym, ys)
         bad = [i for i, (g, w) in enumerate(zip(got, want)) if g != w]
         pytest.fail(f"{name}: y differs from the oracle's in {len(bad)} rows, first {bad[:8]}")
+    # the bench's timed steps: the same step replayed from a CUDA graph (Problem.capture)
+    prob.y_mag.fill_(-1)
+    prob.y_sign.fill_(7)
+    prob.capture()
+    prob.replay()
+    torch.cuda.synchronize()
+    assert prob.status() == hk.HK_OK
+    ym, ys = hk.to_host(*prob.result())
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(ym).tobytes())
+    h.update(np.ascontiguousarray(ys).tobytes())
+    assert h.hexdigest() == meta["y_sha256"], f"{name}: graph-replayed y differs from the oracle's"

@@ -538,6 +538,7 @@ int32_t hk_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_
 
 int32_t hk_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t flags,
                           void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_workspace_init");
     if (!ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, flags, &pl);
@@ -563,6 +564,7 @@ int32_t hk_batch_workspace_size(int32_t kind, int64_t m, int64_t n, int32_t P, i
 
 int32_t hk_batch_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
                                 void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_batch_workspace_init");
     if (!ws || ((uintptr_t)ws & 255) != 0 || nvec < 1) return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, m, n, P, HK_WS_PREPARED, &pl);
@@ -582,6 +584,7 @@ int32_t hk_batch_workspace_init(int32_t kind, int64_t m, int64_t n, int32_t P, i
 int32_t hk_matvec_prepared_batch(int32_t kind, int64_t m, int64_t n, int32_t P, int32_t nvec,
                                  const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
                                  int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_matvec_prepared_batch");
     if (!x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0 ||
         ((uintptr_t)x_mag & 15) != 0 || nvec < 1 || nvec > 65535)
         return HK_EINVAL;
@@ -635,6 +638,7 @@ int32_t hk_workspace_status(void *ws, void *stream, int32_t *data_status) {
 int32_t hk_hankel_matvec(int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
                          const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
                          int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_hankel_matvec");
     return run_matvec(HK_HANKEL, n, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
                       ws_bytes, stream);
 }
@@ -642,6 +646,7 @@ int32_t hk_hankel_matvec(int64_t n, int32_t P, const uint64_t *a_mag, const int8
 int32_t hk_toeplitz_matvec(int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
                            const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
                            int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_toeplitz_matvec");
     return run_matvec(HK_TOEPLITZ, n, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
                       ws_bytes, stream);
 }
@@ -649,6 +654,7 @@ int32_t hk_toeplitz_matvec(int64_t n, int32_t P, const uint64_t *a_mag, const in
 int32_t hk_circulant_matvec(int64_t n, int32_t P, const uint64_t *c_mag, const int8_t *c_sign,
                             const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
                             int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_circulant_matvec");
     return run_matvec(HK_CIRCULANT, n, n, P, c_mag, c_sign, x_mag, x_sign, y_mag, y_sign, ws,
                       ws_bytes, stream);
 }
@@ -656,6 +662,7 @@ int32_t hk_circulant_matvec(int64_t n, int32_t P, const uint64_t *c_mag, const i
 int32_t hk_matvec_rounded(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                           const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
                           uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_matvec_rounded");
     return run_matvec(kind, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws, ws_bytes,
                       stream, HK_STAGE_ALL, true);
 }
@@ -664,6 +671,7 @@ int32_t hk_hankel_rect_matvec(int64_t m, int64_t n, int32_t P, const uint64_t *a
                               const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
                               uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes,
                               void *stream) {
+    HK_NVTX("hk_hankel_rect_matvec");
     return run_matvec(HK_HANKEL, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,
                       ws_bytes, stream);
 }
@@ -672,6 +680,7 @@ int32_t hk_matvec_host(int32_t kind, int64_t m, int64_t n, int32_t P, const uint
                        const int8_t *a_sign_host, const uint64_t *x_mag_host,
                        const int8_t *x_sign_host, uint64_t *y_mag_host, int8_t *y_sign_host,
                        void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_matvec_host");
     if (!a_mag_host || !a_sign_host || !x_mag_host || !x_sign_host || !y_mag_host ||
         !y_sign_host || !ws)
         return HK_EINVAL;
@@ -767,6 +776,7 @@ int32_t hk_matvec_host_async(int32_t kind, int64_t m, int64_t n, int32_t P,
                              const uint64_t *x_mag_host, const int8_t *x_sign_host,
                              uint64_t *y_mag_host, int8_t *y_sign_host, int32_t *status_host,
                              void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_matvec_host_async");
     if (!a_mag_host || !a_sign_host || !x_mag_host || !x_sign_host || !y_mag_host ||
         !y_sign_host || !status_host || !ws)
         return HK_EINVAL;
@@ -824,6 +834,7 @@ int32_t hk_shard_plan(int32_t kind, int64_t n, int32_t P, int32_t G, hk_shard_in
 
 int32_t hk_shard_workspace_init(int32_t kind, int64_t n, int32_t P, int32_t G, void *ws,
                                 size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_shard_workspace_init");
     if (!ws || ((uintptr_t)ws & 255) != 0 || G < 2) return HK_EINVAL;
     Plan pl;
     int rc = make_plan(kind, n, n, P, 0, &pl, G);
@@ -851,6 +862,7 @@ int32_t hk_hankel_shard_forward(int32_t kind, int64_t n, int32_t P, int32_t G, i
                                 const uint64_t *a_mag, const int8_t *a_sign,
                                 const uint64_t *x_mag, const int8_t *x_sign, uint32_t *send,
                                 void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_hankel_shard_forward");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !send) return HK_EINVAL;
     if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
     Plan pl;
@@ -867,6 +879,7 @@ int32_t hk_hankel_shard_forward(int32_t kind, int64_t n, int32_t P, int32_t G, i
 int32_t hk_hankel_shard_finish(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
                                const uint32_t *recv, uint64_t *y_mag, int8_t *y_sign, void *ws,
                                size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_hankel_shard_finish");
     if (!recv || !y_mag || !y_sign) return HK_EINVAL;
     Plan pl;
     Params prm;
@@ -928,6 +941,7 @@ int32_t hk_hankel_shard_slice(int32_t kind, int64_t n, int32_t P, int32_t G, int
                               const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
                               const int8_t *x_sign, uint32_t *slice_send, void *ws, size_t ws_bytes,
                               void *stream) {
+    HK_NVTX("hk_hankel_shard_slice");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !slice_send) return HK_EINVAL;
     if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
     Plan pl;
@@ -945,6 +959,7 @@ int32_t hk_hankel_shard_slice_p2p(int32_t kind, int64_t n, int32_t P, int32_t G,
                                   const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
                                   const int8_t *x_sign, uint32_t *const *slice_recv_ptrs, void *ws,
                                   size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_hankel_shard_slice_p2p");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !slice_recv_ptrs) return HK_EINVAL;
     if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
     Plan pl;
@@ -965,6 +980,7 @@ int32_t hk_hankel_shard_slice_p2p(int32_t kind, int64_t n, int32_t P, int32_t G,
 int32_t hk_hankel_shard_columns(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
                                 const uint32_t *slice_recv, uint32_t *send, void *ws, size_t ws_bytes,
                                 void *stream) {
+    HK_NVTX("hk_hankel_shard_columns");
     if (!slice_recv || !send) return HK_EINVAL;
     Plan pl;
     Params prm;
@@ -978,6 +994,7 @@ int32_t hk_hankel_shard_columns(int32_t kind, int64_t n, int32_t P, int32_t G, i
 int32_t hk_hankel_shard_columns_p2p(int32_t kind, int64_t n, int32_t P, int32_t G, int32_t g,
                                     const uint32_t *slice_recv, uint32_t *const *recv_ptrs, void *ws,
                                     size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_hankel_shard_columns_p2p");
     if (!slice_recv || !recv_ptrs) return HK_EINVAL;
     Plan pl;
     Params prm;
@@ -998,6 +1015,7 @@ int32_t hk_hankel_shard_forward_p2p(int32_t kind, int64_t n, int32_t P, int32_t 
                                     const uint64_t *x_mag, const int8_t *x_sign,
                                     uint32_t *const *recv_ptrs, void *ws, size_t ws_bytes,
                                     void *stream) {
+    HK_NVTX("hk_hankel_shard_forward_p2p");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !recv_ptrs) return HK_EINVAL;
     if ((((uintptr_t)a_mag | (uintptr_t)x_mag) & 15) != 0) return HK_EINVAL;
     Plan pl;
@@ -1020,6 +1038,7 @@ int32_t hk_hankel_shard_finish_p2p(int32_t kind, int64_t n, int32_t P, int32_t G
                                    const uint32_t *recv, uint64_t *const *y_mag_ptrs,
                                    int8_t *const *y_sign_ptrs, void *ws, size_t ws_bytes,
                                    void *stream) {
+    HK_NVTX("hk_hankel_shard_finish_p2p");
     if (!recv || !y_mag_ptrs || !y_sign_ptrs) return HK_EINVAL;
     Plan pl;
     Params prm;
@@ -1040,6 +1059,7 @@ int32_t hk_hankel_shard_finish_p2p(int32_t kind, int64_t n, int32_t P, int32_t G
 
 int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *a_mag,
                      const int8_t *a_sign, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_prepare_a");
     if (!a_mag || !a_sign || !ws || ((uintptr_t)ws & 255) != 0 || ((uintptr_t)a_mag & 15) != 0)
         return HK_EINVAL;
     Plan pl;
@@ -1064,6 +1084,7 @@ int32_t hk_prepare_a(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64
 int32_t hk_matvec_prepared(int32_t kind, int64_t m, int64_t n, int32_t P, const uint64_t *x_mag,
                            const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *ws,
                            size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_matvec_prepared");
     if (!x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0 ||
         ((uintptr_t)x_mag & 15) != 0)
         return HK_EINVAL;
@@ -1094,6 +1115,7 @@ int32_t hk_matvec_stages(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t
                          const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
                          const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *ws,
                          size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_matvec_stages");
     if (stages == 0 || (stages & ~HK_STAGE_ALL)) return HK_EINVAL;
     return run_matvec(kind, m, n, P, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws, ws_bytes,
                       stream, stages);
@@ -1102,6 +1124,7 @@ int32_t hk_matvec_stages(int32_t kind, int64_t m, int64_t n, int32_t P, uint32_t
 int32_t hk_schoolbook_matvec(int32_t kind, int64_t m, int64_t n, int32_t P,
                              const uint64_t *a_mag, const int8_t *a_sign, const uint64_t *x_mag,
                              const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign, void *stream) {
+    HK_NVTX("hk_schoolbook_matvec");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign) return HK_EINVAL;
     if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || m < 1 || P < 1) return HK_EINVAL;
     if (kind != HK_HANKEL && m != n) return HK_EINVAL;
@@ -1117,6 +1140,7 @@ int32_t hk_karatsuba_matvec(int64_t n, int32_t P, int32_t cutoff, const uint64_t
                             const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign,
                             uint64_t *y_mag, int8_t *y_sign, void *ws, size_t ws_bytes,
                             void *stream) {
+    HK_NVTX("hk_karatsuba_matvec");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws) return HK_EINVAL;
     if (((uintptr_t)ws & 255) != 0) return HK_EINVAL;
     return launch_karatsuba(n, P, cutoff, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws,

@@ -684,6 +684,7 @@ int32_t hk_fft_plan(int32_t kind, int64_t n, int32_t P, hk_fft_plan_info *out) {
 }
 
 int32_t hk_fft_workspace_init(int32_t kind, int64_t n, int32_t P, void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_fft_workspace_init");
     if (!ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;
     FftPlan pl;
     int rc = fft_plan(kind, n, P, &pl);
@@ -707,6 +708,7 @@ int32_t hk_fft_workspace_init(int32_t kind, int64_t n, int32_t P, void *ws, size
 int32_t hk_fft_matvec(int32_t kind, int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
                       const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign,
                       void *ws, size_t ws_bytes, void *stream) {
+    HK_NVTX("hk_fft_matvec");
     if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0)
         return HK_EINVAL;
     FftPlan pl;

@@ -6,7 +6,17 @@
 
 #include "../../include/hk.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing unless a tool is attached
+
 namespace hk {
+
+// NVTX range over one C-ABI call (nsys / ncu --nvtx show the library's phases by entry point)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define HK_NVTX(name) ::hk::NvtxRange hk_nvtx_range_(name)
+
 
 constexpr int kNumPrimes = 5;
 constexpr uint64_t kWsMagic = 0x484b5753504c414eull;  // "HKWSPLAN"

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
 #define HK_K3_ROWS 4   // output rows per K3 tile (N2 <= 1024)
 #endif
 #ifndef HK_K3_BLOCK
-#define HK_K3_BLOCK 320
+#define HK_K3_BLOCK 384  // 96 threads per row, 80 registers, 2 CTAs/SM (320: 96 registers, C3 K3 +5%)
 #endif
 #ifndef HK_K3_GARNER_SLOT
 #define HK_K3_GARNER_SLOT 1  // Garner slot by slot (CRT words at the residue slot) instead of in pairs
@@ -410,8 +410,7 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rown
 #endif
 template <int LOGN2>
 constexpr int k3_rows() { return LOGN2 >= 11 ? 2 : HK_K3_ROWS; }
-// threads per K3 CTA and CTAs per SM: 80 threads per row of the tile (320 for the 2-row tiles of
-// N2 = 2048, HK_K3_BLOCK otherwise)
+// threads per K3 CTA and CTAs per SM: HK_K3_BLOCK (320 for the 2-row tiles of N2 = 2048)
 template <int LOGN2>
 constexpr int k3_threads() { return LOGN2 >= 11 ? 320 : HK_K3_BLOCK; }
 template <int LOGN2>
@@ -1235,11 +1234,14 @@ static int launch_k3(const Params &prm, cudaStream_t st, int64_t nrows) {
 
 // limbs per thread reachable for a slice length 2^LOGN2 (the planner picks the smallest N2 with
 // 2 ceil(P / w) - 1 <= N2, w in {64, 65}; Ly = 2 ceil(P / 64) + 1 <= kK3MaxLy): only these are built
+// (Ly from about N2 / 2 + 1 up to 2 ceil(65 (N2 / 2) / 64) + 1, over TR = threads per row)
+template <int LOGN2> constexpr int k3_tr() { return k3_threads<LOGN2>() / k3_rows<LOGN2>(); }
 template <int LOGN2> constexpr int k3_ch_lo() {
-    return LOGN2 <= 8 ? (LOGN2 == 8 ? 2 : 1) : (LOGN2 == 9 ? 4 : 7);
+    return LOGN2 <= 6 ? 1 : (((1 << LOGN2) / 2 + 1 + k3_tr<LOGN2>() - 1) / k3_tr<LOGN2>() - 1 < 1
+                                 ? 1 : ((1 << LOGN2) / 2 + 1 + k3_tr<LOGN2>() - 1) / k3_tr<LOGN2>() - 1);
 }
 template <int LOGN2> constexpr int k3_ch_hi() {
-    return LOGN2 <= 6 ? 1 : (LOGN2 == 7 ? 2 : (LOGN2 == 8 ? 4 : (LOGN2 == 9 ? 7 : 14)));
+    return ((1 << LOGN2) * 65 / 64 + 3 + k3_tr<LOGN2>() - 1) / k3_tr<LOGN2>();
 }
 template <int LOGN2, int C>
 static int k3_dispatch(const Params &prm, cudaStream_t st, int64_t nrows, int ch) {

@@ -40,8 +40,15 @@ constexpr int k2_threads() {
     if (LOGN1 == 14) return HK_K2_T14;
     return (1 << LOGN1) / 32 < 32 ? 32 : ((1 << LOGN1) / 32 > 512 ? 512 : (1 << LOGN1) / 32);
 }
+#ifndef HK_K2_WARPS_SMALL
+#define HK_K2_WARPS_SMALL 24  // N1 <= 2^13: resident warps per SM asked of the register allocator (0: no
+                              // bound; 24 caps at 80 registers: K2 -9% at C2 and C5 circulant, -4% at C5 Toeplitz)
+#endif
 template <int LOGN1>
-constexpr int k2_min_blocks() { return LOGN1 == 14 ? HK_K2_MINB14 : 1; }
+constexpr int k2_min_blocks() {
+    return LOGN1 == 14 ? HK_K2_MINB14
+                       : (LOGN1 < 14 && HK_K2_WARPS_SMALL > 0 ? HK_K2_WARPS_SMALL * 32 / k2_threads<LOGN1>() : 1);
+}
 
 template <int LOGN>
 struct ColPlan {

@@ -101,6 +101,11 @@ constexpr int k1_row_stride() {  // = 4 (mod 32): transposed [row][sigma] tiles 
 #define HK_K1_MINB 3
 #endif
 constexpr int kK1Rows = HK_K1_ROWS;
+#ifndef HK_K1_MINB_SMALL
+#define HK_K1_MINB_SMALL 5  // resident CTAs per SM for N2 <= 512 (128-thread CTAs; 3 -> 5: C5 K1 -4%)
+#endif
+template <int LOGN2>
+constexpr int k1_minb() { return LOGN2 <= 9 ? HK_K1_MINB_SMALL : HK_K1_MINB; }
 #ifndef HK_K1_TMA
 #define HK_K1_TMA 1  // stage the limb tile with one TMA bulk copy (else per-thread cp.async)
 #endif
@@ -125,7 +130,7 @@ constexpr int k1_threads() {
 // Block b holds the transform outputs at bit-reversed positions [b N2 / G, (b + 1) N2 / G), the
 // frequencies congruent to bitrev(b) mod G.
 template <int LOGN2, int GSEL>  // GSEL = gamma (coset shards keep N2 / 2^gamma outputs), -1: sliced shards
-__global__ void __launch_bounds__(k1_threads<LOGN2>(), HK_K1_MINB) k1_slice_rowntt(Params prm, int tiles_a) {
+__global__ void __launch_bounds__(k1_threads<LOGN2>(), k1_minb<LOGN2>()) k1_slice_rowntt(Params prm, int tiles_a) {
     constexpr int GAMMA = GSEL < 0 ? 0 : GSEL;
     constexpr bool SLICED = GSEL < 0;
     constexpr int N2 = 1 << LOGN2;
@@ -1099,7 +1104,7 @@ static int launch_rows_g(const Params &prm0, cudaStream_t st, int tile0, int nti
         else
             return HK_ECUDA;
     }
-    prm.k1_prime_split = (int64_t)ntiles * prm.nvec * kNumPrimes <= (int64_t)HK_K1_MINB * nsm ? 1 : 0;
+    prm.k1_prime_split = (int64_t)ntiles * prm.nvec * kNumPrimes <= (int64_t)k1_minb<LOGN2>() * nsm ? 1 : 0;
     k1_slice_rowntt<LOGN2, GAMMA><<<dim3((unsigned)ntiles, (unsigned)prm.nvec, prm.k1_prime_split ? kNumPrimes : 1),
                                      k1_threads<LOGN2>(), smem1, st>>>(prm, ga);
     return check_launch();

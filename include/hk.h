@@ -410,6 +410,25 @@ int32_t hk_fft_matvec(int32_t kind, int64_t n, int32_t P,
                       uint64_t *y_mag, int8_t *y_sign,
                       void *ws, size_t ws_bytes, void *stream);
 
+/* F3 accuracy study (second half; "whether the loss of accuracy occurs in
+ * practice"): the same plan, workspace and matvec with the digit width FORCED to w (w = 0: the
+ * proven planner above, identical to hk_fft_plan / _workspace_init / _matvec).  For w wider than
+ * the proven one the Percival bound in info.bound exceeds 1/2 and the result is NOT guaranteed
+ * exact -- these entry points exist to measure where exactness is actually lost.  HK_EINVAL for
+ * w outside [0, 30]; HK_EUNSUPPORTED when the digit FFT would exceed N2 = 8192 or a coefficient
+ * could reach 2^62.  A workspace initialised for one w is rejected (data status HK_EINVAL) by a
+ * call with another.  max_residual: optional DEVICE pointer to one 8-byte-aligned double holding
+ * a non-negative value (the caller zeroes it); the call raises it to the largest |v - rint(v)|
+ * over every scaled output coefficient v it rounds (the distance the bound is about). */
+int32_t hk_fft_plan_w(int32_t kind, int64_t n, int32_t P, int32_t w, hk_fft_plan_info *out);
+int32_t hk_fft_workspace_init_w(int32_t kind, int64_t n, int32_t P, int32_t w, void *ws,
+                                size_t ws_bytes, void *stream);
+int32_t hk_fft_matvec_w(int32_t kind, int64_t n, int32_t P, int32_t w,
+                        const uint64_t *a_mag, const int8_t *a_sign,
+                        const uint64_t *x_mag, const int8_t *x_sign,
+                        uint64_t *y_mag, int8_t *y_sign,
+                        void *ws, size_t ws_bytes, void *stream, double *max_residual);
+
 #ifdef __cplusplus
 }
 #endif

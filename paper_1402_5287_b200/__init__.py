@@ -124,6 +124,9 @@ def _load():
         "hk_fft_plan": (i32, [i32, i64, i32, ctypes.POINTER(FftPlanInfo)]),
         "hk_fft_workspace_init": (i32, [i32, i64, i32, vp, sz, vp]),
         "hk_fft_matvec": (i32, [i32, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]),
+        "hk_fft_plan_w": (i32, [i32, i64, i32, i32, ctypes.POINTER(FftPlanInfo)]),
+        "hk_fft_workspace_init_w": (i32, [i32, i64, i32, i32, vp, sz, vp]),
+        "hk_fft_matvec_w": (i32, [i32, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -142,7 +145,8 @@ EXPORTED = ("hk_limbs", "hk_out_limbs", "hk_status_string", "hk_plan", "hk_works
             "hk_matvec_rounded", "hk_hankel_shard_forward_p2p", "hk_hankel_shard_finish_p2p",
             "hk_fft_plan", "hk_fft_workspace_init", "hk_fft_matvec", "hk_batch_workspace_size",
             "hk_batch_workspace_init", "hk_matvec_prepared_batch", "hk_hankel_shard_slice",
-            "hk_hankel_shard_slice_p2p", "hk_hankel_shard_columns", "hk_hankel_shard_columns_p2p")
+            "hk_hankel_shard_slice_p2p", "hk_hankel_shard_columns", "hk_hankel_shard_columns_p2p",
+            "hk_fft_plan_w", "hk_fft_workspace_init_w", "hk_fft_matvec_w")
 STAGE_SLICE_ROWS, STAGE_COLUMNS, STAGE_FINISH, STAGE_ALL = 1, 2, 4, 7
 
 
@@ -807,32 +811,39 @@ def karatsuba_matvec(a_mag, a_sign, x_mag, x_sign, P, cutoff: int = 8, out=None,
 
 
 # ---- F3: the paper's decomposition approach with a double-precision FFT (exact by Percival's bound)
-def fft_plan(kind: int, n: int, P: int) -> dict:
-    """The FP64-FFT plan (digit width w, lengths, Percival bound); pure host call."""
+def fft_plan(kind: int, n: int, P: int, w: int = 0) -> dict:
+    """The FP64-FFT plan (digit width w, lengths, Percival bound); pure host call.  w > 0 forces
+    the digit width (F3 accuracy study, hk_fft_plan_w: the bound may then exceed 1/2)."""
     info = FftPlanInfo()
-    _check(_lib.hk_fft_plan(int(kind), int(n), int(P), ctypes.byref(info)), "hk_fft_plan")
+    _check(_lib.hk_fft_plan_w(int(kind), int(n), int(P), int(w), ctypes.byref(info)), "hk_fft_plan_w")
     return info.as_dict()
 
 
 class FftWorkspace:
-    """Device workspace of the F3 path (twiddle tables, carry table, 2 x N1 x N2 complex doubles)."""
+    """Device workspace of the F3 path (twiddle tables, carry table, 2 x N1 x N2 complex doubles);
+    w > 0: the forced-width plan of the accuracy study."""
 
-    def __init__(self, kind, n, P, device=None, stream=None):
+    def __init__(self, kind, n, P, device=None, stream=None, w=0):
         import torch
-        self.kind, self.n, self.P = int(kind), int(n), int(P)
-        self.info = fft_plan(kind, n, P)
+        self.kind, self.n, self.P, self.w = int(kind), int(n), int(P), int(w)
+        self.info = fft_plan(kind, n, P, w)
         self.nbytes = int(self.info["ws_bytes"])
         self.buf = torch.empty(self.nbytes + 256, dtype=torch.uint8,
                                device=device or torch.device("cuda", torch.cuda.current_device()))
         self.ptr = (self.buf.data_ptr() + 255) & ~255
-        _check(_lib.hk_fft_workspace_init(self.kind, self.n, self.P, self.ptr, self.nbytes,
-                                          _stream_ptr(stream)), "hk_fft_workspace_init")
+        _check(_lib.hk_fft_workspace_init_w(self.kind, self.n, self.P, self.w, self.ptr, self.nbytes,
+                                            _stream_ptr(stream)), "hk_fft_workspace_init_w")
 
     status = Workspace.status
 
 
-def fft_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, out=None, ws=None, stream=None, check=True):
-    """y = A x exactly through the FP64 FFT path (hk_fft_matvec): same layouts as matvec()."""
+def fft_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, out=None, ws=None, stream=None, check=True,
+               w=0, residual=None):
+    """y = A x exactly through the FP64 FFT path (hk_fft_matvec): same layouts as matvec().
+
+    Accuracy study (hk_fft_matvec_w): ``w`` > 0 forces the digit width -- past the proven one the
+    result is not guaranteed exact; ``residual``, a zeroed float64 CUDA tensor of one element, is
+    raised to the largest |v - rint(v)| over the rounded output coefficients."""
     import torch
     n = int(x_mag.shape[0])
     L, Ly = limbs(P), out_limbs(P)
@@ -847,11 +858,14 @@ def fft_matvec(kind, a_mag, a_sign, x_mag, x_sign, P, out=None, ws=None, stream=
     args += [_dev_ptr(out[0], _mag_dtypes(), (n, Ly), "y_mag"),
              _dev_ptr(out[1], (torch.int8,), (n,), "y_sign")]
     if ws is None:
-        ws = FftWorkspace(kind, n, P, stream=stream)
-    if (ws.kind, ws.n, ws.P) != (int(kind), n, int(P)):
+        ws = FftWorkspace(kind, n, P, stream=stream, w=w)
+    if (ws.kind, ws.n, ws.P, ws.w) != (int(kind), n, int(P), int(w)):
         raise ValueError("FFT workspace was initialised for a different problem")
-    _check(_lib.hk_fft_matvec(int(kind), n, int(P), *args, ws.ptr, ws.nbytes, _stream_ptr(stream)),
-           "hk_fft_matvec")
+    rp = None
+    if residual is not None:
+        rp = _dev_ptr(residual, (torch.float64,), (1,), "residual")
+    _check(_lib.hk_fft_matvec_w(int(kind), n, int(P), int(w), *args, ws.ptr, ws.nbytes, _stream_ptr(stream),
+                                rp), "hk_fft_matvec_w")
     if check:
         _check(ws.status(stream), "hk_fft_matvec data status")
     return out

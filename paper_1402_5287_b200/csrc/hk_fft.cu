@@ -65,6 +65,8 @@ struct FftParams {
     const int8_t *a_sign, *x_sign;
     uint64_t *y_mag;
     int8_t *y_sign;
+    unsigned long long *resid;     // F3 accuracy study: max |v - rint(v)| over the coefficients
+                                   // (bits of a non-negative double; nullptr in the product path)
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -331,10 +333,18 @@ __global__ void __launch_bounds__(kFftThreads) f3_finish(FftParams prm) {
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         __syncthreads();
         CDit<LOGN2, 0>::run(cs, 1, 0, prm.tw2);
+        double rmax = 0.0;
         for (int t = tid; t < N2; t += T) {
-            const int64_t c = (int64_t)rint(cs[cpad(t)].x * scale);
+            const double v = cs[cpad(t)].x * scale, r = rint(v);
+            const int64_t c = (int64_t)r;
+            rmax = fmax(rmax, fabs(v - r));
             if (rep == 0) coef[t] = (uint64_t)c + (t < S2 ? (1ull << prm.cb) : 0ull);
             else coef[t] += (uint64_t)c;
+        }
+        if (prm.resid) {  // study only: one atomic per warp (non-negative doubles order as integers)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+            if (lane == 0) atomicMax(prm.resid, (unsigned long long)__double_as_longlong(rmax));
         }
         __syncthreads();
     }
@@ -450,17 +460,20 @@ long double percival_factor(int k, long double eps, long double beta) {
     return expm1l(lg);
 }
 
-uint64_t fft_hash(int32_t kind, int64_t n, int32_t P) {
+uint64_t fft_hash(int32_t kind, int64_t n, int32_t P, int32_t w) {
     uint64_t h = 1469598103934665603ull ^ 0x464654ull;
     auto mix = [&](uint64_t v) {
         for (int i = 0; i < 8; ++i) { h ^= (v >> (8 * i)) & 0xff; h *= 1099511628211ull; }
     };
-    mix((uint64_t)kind); mix((uint64_t)n); mix((uint64_t)P);
+    mix((uint64_t)kind); mix((uint64_t)n); mix((uint64_t)P); mix((uint64_t)w);
     return h;
 }
 
-int fft_plan(int32_t kind, int64_t n, int32_t P, FftPlan *pl) {
-    if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || P < 1) return HK_EINVAL;
+// w_force = 0: the widest w whose Percival bound is <= 0.49 (the exact product path);
+// w_force > 0 (F3 accuracy study, hk_fft_plan_w): that digit width, whatever its bound (reported),
+// as long as the transform fits and |coefficient| < 2^62 (the bias / carry arithmetic)
+int fft_plan(int32_t kind, int64_t n, int32_t P, FftPlan *pl, int32_t w_force = 0) {
+    if (kind < HK_HANKEL || kind > HK_CIRCULANT || n < 1 || P < 1 || w_force < 0 || w_force > 30) return HK_EINVAL;
     std::memset(pl, 0, sizeof(*pl));
     hk_fft_plan_info &in = pl->info;
     in.kind = kind; in.P = P; in.m = n; in.n = n;
@@ -490,7 +503,8 @@ int fft_plan(int32_t kind, int64_t n, int32_t P, FftPlan *pl) {
     in.beta = std::ldexp(1.0, -52);
     const long double rows_a = (long double)in.a_count;
     bool found = false;
-    for (int w = 30; w >= 2 && !found; --w) {
+    for (int w = w_force ? w_force : 30; w >= 2 && !found; --w) {
+        if (w_force && w != w_force) break;
         const int64_t Ls = (P + w - 1) / w + 1;
         int lg2 = kFftMinLog;
         while ((int64_t(1) << lg2) < 2 * Ls - 1) ++lg2;
@@ -500,7 +514,7 @@ int fft_plan(int32_t kind, int64_t n, int32_t P, FftPlan *pl) {
         const long double norm = sqrtl(rows_a * (long double)n) * (long double)Ls * dmax * dmax;
         const long double B = norm * percival_factor(k, in.eps, in.beta);
         const long double cmax = (long double)n * (long double)Ls * dmax * dmax;  // |c_s| bound
-        if (B <= 0.49L && cmax < ldexpl(1.0L, 52)) {
+        if (w_force ? cmax < ldexpl(1.0L, 62) : (B <= 0.49L && cmax < ldexpl(1.0L, 52))) {
             in.w = w; in.Ls = (int32_t)Ls; in.log_n2 = lg2; in.bound = (double)B;
             int cb = 0;
             while (ldexpl(1.0L, cb) <= cmax) ++cb;
@@ -531,7 +545,7 @@ void fft_fill(const FftPlan &pl, void *ws, FftParams *prm) {
     prm->m = in.m; prm->n = in.n; prm->a_count = in.a_count; prm->out_off = pl.out_off;
     prm->reverse_out = pl.reverse_out; prm->x_reversed = pl.x_reversed; prm->fold = pl.fold;
     prm->cb = pl.cb;
-    prm->hash = fft_hash(in.kind, in.n, in.P);
+    prm->hash = fft_hash(in.kind, in.n, in.P, in.w);
     char *base = (char *)ws;
     prm->hdr = (WsHeader *)base;
     prm->tw1 = (const double2 *)(base + pl.off_tw1);
@@ -674,20 +688,25 @@ using namespace hk;
 
 extern "C" {
 
-int32_t hk_fft_plan(int32_t kind, int64_t n, int32_t P, hk_fft_plan_info *out) {
+int32_t hk_fft_plan_w(int32_t kind, int64_t n, int32_t P, int32_t w, hk_fft_plan_info *out) {
     if (!out) return HK_EINVAL;
     FftPlan pl;
-    const int rc = fft_plan(kind, n, P, &pl);
+    const int rc = fft_plan(kind, n, P, &pl, w);
     if (rc) return rc;
     *out = pl.info;
     return HK_OK;
 }
 
-int32_t hk_fft_workspace_init(int32_t kind, int64_t n, int32_t P, void *ws, size_t ws_bytes, void *stream) {
+int32_t hk_fft_plan(int32_t kind, int64_t n, int32_t P, hk_fft_plan_info *out) {
+    return hk_fft_plan_w(kind, n, P, 0, out);
+}
+
+int32_t hk_fft_workspace_init_w(int32_t kind, int64_t n, int32_t P, int32_t w, void *ws, size_t ws_bytes,
+                                void *stream) {
     HK_NVTX("hk_fft_workspace_init");
     if (!ws || ((uintptr_t)ws & 255) != 0) return HK_EINVAL;
     FftPlan pl;
-    int rc = fft_plan(kind, n, P, &pl);
+    int rc = fft_plan(kind, n, P, &pl, w);
     if (rc) return rc;
     if (ws_bytes < pl.info.ws_bytes) return HK_ENOMEM;
     FftParams prm;
@@ -705,14 +724,19 @@ int32_t hk_fft_workspace_init(int32_t kind, int64_t n, int32_t P, void *ws, size
     return fft_check_launch();
 }
 
-int32_t hk_fft_matvec(int32_t kind, int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
-                      const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign,
-                      void *ws, size_t ws_bytes, void *stream) {
+int32_t hk_fft_workspace_init(int32_t kind, int64_t n, int32_t P, void *ws, size_t ws_bytes, void *stream) {
+    return hk_fft_workspace_init_w(kind, n, P, 0, ws, ws_bytes, stream);
+}
+
+int32_t hk_fft_matvec_w(int32_t kind, int64_t n, int32_t P, int32_t w, const uint64_t *a_mag,
+                        const int8_t *a_sign, const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag,
+                        int8_t *y_sign, void *ws, size_t ws_bytes, void *stream, double *max_residual) {
     HK_NVTX("hk_fft_matvec");
-    if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0)
+    if (!a_mag || !a_sign || !x_mag || !x_sign || !y_mag || !y_sign || !ws || ((uintptr_t)ws & 255) != 0 ||
+        ((uintptr_t)max_residual & 7) != 0)
         return HK_EINVAL;
     FftPlan pl;
-    int rc = fft_plan(kind, n, P, &pl);
+    int rc = fft_plan(kind, n, P, &pl, w);
     if (rc) return rc;
     if (ws_bytes < pl.info.ws_bytes) return HK_ENOMEM;
     const size_t Ly = pl.info.Ly, L = pl.info.L, na = pl.info.a_count;
@@ -724,9 +748,17 @@ int32_t hk_fft_matvec(int32_t kind, int64_t n, int32_t P, const uint64_t *a_mag,
     fft_fill(pl, ws, &prm);
     prm.a_mag = a_mag; prm.a_sign = a_sign; prm.x_mag = x_mag; prm.x_sign = x_sign;
     prm.y_mag = y_mag; prm.y_sign = y_sign;
+    prm.resid = reinterpret_cast<unsigned long long *>(max_residual);
     cudaStream_t st = (cudaStream_t)stream;
     if (cudaMemsetAsync(&prm.hdr->status, 0, sizeof(int32_t), st) != cudaSuccess) return HK_ECUDA;
     return fft_run(prm, st);
+}
+
+int32_t hk_fft_matvec(int32_t kind, int64_t n, int32_t P, const uint64_t *a_mag, const int8_t *a_sign,
+                      const uint64_t *x_mag, const int8_t *x_sign, uint64_t *y_mag, int8_t *y_sign,
+                      void *ws, size_t ws_bytes, void *stream) {
+    return hk_fft_matvec_w(kind, n, P, 0, a_mag, a_sign, x_mag, x_sign, y_mag, y_sign, ws, ws_bytes, stream,
+                           nullptr);
 }
 
 }  // extern "C"

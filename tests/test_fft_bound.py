@@ -138,3 +138,46 @@ def test_radix2_fft_error_below_bound():
             exact[(i + j) % N1] += np.convolve(A[i, :Ls], X[j, :Ls], mode="full").tolist() + [0] * (N2 - 2 * Ls + 1)
     err = np.abs(Z - exact).max()
     assert err < ref["bound"] < 0.5, (err, ref["bound"])
+
+
+def forced_bound(kind: int, n: int, P: int, w: int):
+    """Percival's bound at a FORCED digit width w (the accuracy study's plans), 60-digit decimal."""
+    a_count = n if kind == gen.CIRCULANT else 2 * n - 1
+    if kind == gen.CIRCULANT and n & (n - 1) == 0 and n >= 32:
+        lg1 = log2ceil(n)
+    else:
+        lg1 = max(5, log2ceil(2 * n - 1 if kind == gen.CIRCULANT else a_count))
+    Ls = -(-P // w) + 1
+    lg2 = max(5, log2ceil(2 * Ls - 1))
+    d = Decimal(2) ** (w - 1)
+    return dict(Ls=Ls, log_n1=lg1, log_n2=lg2,
+                bound=float(Decimal(a_count * n).sqrt() * Ls * d * d * percival_factor(lg1 + lg2)),
+                fits=lg2 <= 13 and n * Ls * d * d < Decimal(2) ** 62)
+
+
+def test_forced_width_plans():
+    """hk_fft_plan_w (F3 accuracy study): w = 0 is the proven plan; a forced w reports that width's
+    Percival bound (a restatement of the theorem, 60 digits), past 1/2 for widths wider than the
+    proven one, and refuses widths whose digit FFT or coefficients do not fit."""
+    import paper_1402_5287_b200 as hk
+    for kind, n, P in [(0, 8000, 33216), (0, 1024, 33216), (1, 4096, 16608), (2, 64, 3328)]:
+        proven = hk.fft_plan(kind, n, P)
+        assert hk.fft_plan(kind, n, P, w=0) == proven
+        assert hk.fft_plan(kind, n, P, w=proven["w"]) == proven
+        prev = 0.0
+        for w in range(2, 31):
+            ref = forced_bound(kind, n, P, w)
+            if not ref["fits"]:
+                with pytest.raises(hk.HKError):
+                    hk.fft_plan(kind, n, P, w=w)
+                continue
+            got = hk.fft_plan(kind, n, P, w=w)
+            assert (got["w"], got["Ls"], got["log_n1"], got["log_n2"]) == (w, ref["Ls"], ref["log_n1"], ref["log_n2"])
+            assert abs(got["bound"] - ref["bound"]) <= 1e-9 * ref["bound"]
+            assert got["bound"] > prev  # the bound grows with the digit width
+            prev = got["bound"]
+            if w > proven["w"]:
+                assert got["bound"] > 0.49
+    for bad in (-1, 31):
+        with pytest.raises(hk.HKError):
+            hk.fft_plan(0, 64, 3328, w=bad)

@@ -122,3 +122,32 @@ def test_workspace_reuse(hk):
         x, sx = hk.to_device(xm, xsg)
         got = hk.to_host(*hk.fft_matvec(0, a, sa, x, sx, P, ws=ws))
         assert_same(got, oracle.matvec(0, P, am, asg, xm, xsg), f"reuse seed={seed}")
+
+
+def test_forced_width_study_path(hk):
+    """F3 accuracy study entry points (hk_fft_matvec_w): at the proven width the forced-w path is the
+    product path (same y, the oracle's) and its measured max |v - rint(v)| stays under the Percival
+    bound; at wider widths, whenever every residual is below 1/2 the rounded coefficients are the
+    exact integers, so y must still equal the oracle's (a residual >= 1/2 is allowed to break it)."""
+    kind, n, P = 0, 96, 3328
+    am, asg, xm, xsg = gen.make_inputs(kind, n, P, seed=11)
+    want = oracle.matvec(kind, P, am, asg, xm, xsg)
+    a, sa = hk.to_device(am, asg)
+    x, sx = hk.to_device(xm, xsg)
+    proven = hk.fft_plan(kind, n, P)
+    for w in (proven["w"], proven["w"] + 2, proven["w"] + 4, proven["w"] + 8):
+        info = hk.fft_plan(kind, n, P, w=w)
+        res = torch.zeros(1, dtype=torch.float64, device=a.device)
+        ym, ys = hk.fft_matvec(kind, a, sa, x, sx, P, w=w, residual=res)
+        torch.cuda.synchronize()
+        r = float(res.item())
+        got = hk.to_host(ym, ys)
+        if w == proven["w"]:
+            assert 0.0 < r <= info["bound"] < 0.5, (w, r, info["bound"])
+            assert_same(got, want, f"proven w={w}")
+        elif r < 0.5:
+            assert_same(got, want, f"w={w} residual {r}")
+    # a workspace initialised for one width is refused by a call with another
+    ws = hk.FftWorkspace(kind, n, P, w=proven["w"] + 2)
+    with pytest.raises(ValueError):
+        hk.fft_matvec(kind, a, sa, x, sx, P, ws=ws)

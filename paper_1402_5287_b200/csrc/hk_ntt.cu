@@ -25,8 +25,9 @@ namespace hk {
 
 // Raise a kernel's dynamic shared-memory limit once per (kernel, size) instead of on every launch
 // (the attribute call is host time that small problems feel; one device per process).
+// The default limit covers static + dynamic <= 48 KB; beyond that the attribute must be raised.
 static int ensure_smem(const void *kern, size_t smem) {
-    if (smem <= 48 * 1024) return HK_OK;
+    if (smem <= 32 * 1024) return HK_OK;  // every kernel here has < 16 KB of static shared memory
     static std::mutex mu;
     static std::unordered_map<const void *, size_t> done;
     std::lock_guard<std::mutex> lk(mu);
@@ -409,6 +410,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), k1_minb<LOGN2>()) k1_slic
 #ifndef HK_K3_GARNER_X2
 #define HK_K3_GARNER_X2 0  // two Garner slots per thread per round
 #endif
+#ifndef HK_K3_FUSED
+#define HK_K3_FUSED 1  // Garner fused into the carry gather (no separate CRT phase, no lookbehind): C3 K3 -1.5%
+#endif
 #ifndef HK_K3_SKIP
 #define HK_K3_SKIP 0  // dev timing only (wrong results): 1 skips the inverse NTTs, 2 Garner, 4 the
                       // gather, 8 the Y^ load, 16 the y store
@@ -674,6 +678,9 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
 #if !(HK_K3_SKIP & 1)
     K3Dit<LOGN2, 0>::run(sm, prm);
 #endif
+    // fused (HK_K3_FUSED, chunks of >= 3 limbs): each coefficient is converted inside the carry
+    // gather (c) below instead
+    constexpr bool kFused = HK_K3_FUSED && HK_K3_V2 && CH >= 3;
 #if HK_K3_SKIP & 2
 #elif HK_K3_GARNER_X2 && HK_K3_V2
     // (b) Garner CRT in place, two slots per thread per round (independent chains interleave)
@@ -707,7 +714,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     // (b) Garner CRT in place, slot by slot: coefficient s lives at sigma = (N2 - s) mod N2 and its
     // CRT words overwrite its own residues there, so any thread may take any slot (R N2 slots over
     // the block: no pairing, no remainder round of pairs)
-    for (int it = tid; it < R * N2; it += T) {
+    for (int it = tid; it < (kFused ? 0 : R * N2); it += T) {
         const int r = it % R, sg = it / R;
         uint32_t ra[kNumPrimes], ca[kNumPrimes];
 #pragma unroll
@@ -745,95 +752,182 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
         }
     }
 #endif
-    __syncthreads();
+    if constexpr (!kFused) __syncthreads();
 
 #if HK_K3_V2
-    // (c) v2: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R).  Coefficient s
-    // (unsigned C'' < M < 2^155, five words at its residue slot) sits at limb q(s) = floor(w s / 64)
-    // shifted by w s mod 64 (w = 65: s = 64 a + b -> q = 65 a + b, shift b; w = 64: q = s).  The
-    // thread walks positions q = l0 - 3 .. l0 + CH - 1 once, keeping the partial sums of the next
-    // three limbs in registers: limb q is complete after the coefficient at q, and then gets -K's
-    // limb.  u = limb value mod 2^64, e = carries out of those additions (<= 4, added to limb q + 1
-    // below).
     const int Ly = prm.Ly;
     const int r = tid % R, k = tid / R, lane_r = lane / R;  // lane_r: position among the row's lanes
     const int l0 = k * CH;
     const uint32_t *smr = sm + r;
-    const uint32_t *qmap = prm.qmap + l0;  // entry j: position qq = l0 - 3 + j (padded past Ly)
-    const uint64_t *negk = prm.negK + l0;  // zero-padded past Ly
-    // pending partial sums of limbs q, q + 1, q + 2 as 32-bit halves, and their carry counts
-    uint32_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, a2l = 0, a2h = 0;
-    int n0 = 0, n1 = 0, n2 = 0;
-    // Limb c of the chunk: v_c = its sum mod 2^64, e_c = carries out of that sum (<= 4).  Binary
-    // lookahead on w_c = v_c + e_(c-1): w_c generates g_c (carry out) or propagates p_c
-    // (w_c = 2^64 - 1); carry into c + 1 = g_c | (p_c & carry into c).  For c >= 1 e_(c-1) is this
-    // thread's, so w_c, g_c, p_c are formed here; limb 0 waits for the previous chunk's e.
-    uint64_t u[CH];
-    uint32_t v0l = 0, v0h = 0;       // limb 0 before e_in
-    int e_prev = 0;
-    uint32_t gbits = 0, pbits = 0;
-    uint32_t Gt = 0, Pt = 1;         // (G, P) of limbs 1 .. c
-#if HK_K3_SKIP & 4
+    uint64_t u[CH];                  // limb values of the chunk
+    uint32_t gbits = 0, pbits = 0;   // per-limb generate / propagate bits
+    uint32_t Gt = 0, Pt = 1;         // the chunk's composed (G, P)
+    __shared__ int s_neg[R], s_zmin[R];
+    if constexpr (kFused) {
+        // (c) v3, Garner fused into the gather: thread t owns limbs [k CH, k CH + CH) of row r = t % R
+        // (k = t / R) and converts exactly the coefficients that sit at those limbs (the residues of
+        // coefficient s at its slot -> garner2 -> five words C'' < M), shifting each into the partial
+        // sums of limbs q .. q + 3 (w = 65: q = 65 a + b for s = 64 a + b, shift b; w = 64: q = s).
+        // Limb l0 + c is complete after position l0 + c except for the spill-over of the previous
+        // chunk's last three coefficients into limbs l0 .. l0 + 2: that arrives through shared memory
+        // (the previous thread's pending partial sums and carry counts) instead of being recomputed.
+        const uint32_t *qmap = prm.qmap + l0 + 3;  // entry c: position l0 + c (padded past Ly)
+        const uint64_t *negk = prm.negK + l0;      // zero-padded past Ly
+        constexpr uint32_t kZeroSlot = (uint32_t)R;  // LY::idx(0, 1, 0) = pad(1) R: s = N2 - 1, never a coefficient
+        static_assert(CH <= 16, "4-bit carry counts for at most 16 limbs per thread");
+        uint32_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, a2l = 0, a2h = 0;
+        int n0 = 0, n1 = 0, n2 = 0;
+        uint64_t ecnt = 0;              // e_c: carries out of those sums, 4 bits per limb
 #pragma unroll
-    for (int c = 0; c < CH; ++c) u[c] = smr[c * R];
+        for (int c = 0; c < CH; ++c) {
+            const uint32_t qm = __ldg(qmap + c);
+            const uint32_t o = qm >> 6, sh = qm & 63u;
+            uint32_t ra[kNumPrimes], cw[kNumPrimes];
 #pragma unroll
-    for (int j = 0; j < 0; ++j) {
-#else
-#pragma unroll
-    for (int j = 0; j < CH + 3; ++j) {
-#endif
-        const uint32_t qm = __ldg(qmap + j);
-        const uint32_t o = qm >> 6, sh = qm & 63u;
-        const uint32_t w0 = smr[o], w1 = smr[LY::PS + o], w2 = smr[2 * LY::PS + o],
-                       w3 = smr[3 * LY::PS + o], w4 = smr[4 * LY::PS + o];
-        const uint32_t bs = sh & 31u;
-        const uint32_t h0 = w0 << bs, h1 = __funnelshift_l(w0, w1, bs), h2 = __funnelshift_l(w1, w2, bs),
-                       h3 = __funnelshift_l(w2, w3, bs), h4 = __funnelshift_l(w3, w4, bs),
-                       h5 = __funnelshift_l(w4, 0u, bs);
-        const bool up = sh >= 32u;  // the image starts one 32-bit word higher
-        const uint32_t s0 = sel32(up, 0u, h0), s1 = sel32(up, h0, h1), s2 = sel32(up, h1, h2),
-                       s3 = sel32(up, h2, h3), s4 = sel32(up, h3, h4), s5 = sel32(up, h4, h5),
-                       s6 = sel32(up, h5, 0u);
-        add64_count(a0l, a0h, n0, s0, s1);  // limb q
-        add64_count(a1l, a1h, n1, s2, s3);  // limb q + 1
-        add64_count(a2l, a2h, n2, s4, s5);  // limb q + 2 (s6 -> limb q + 3, below)
-        if (j >= 3) {  // limb l = qq is complete: add -K's limb
-            const int c = j - 3;
+            for (int kp = 0; kp < kNumPrimes; ++kp) ra[kp] = smr[kp * LY::PS + o];
+            garner2(ra, prm, cw);
+            const bool zs = o == kZeroSlot;
+            const uint32_t w0 = zs ? 0u : cw[0], w1 = zs ? 0u : cw[1], w2 = zs ? 0u : cw[2],
+                           w3 = zs ? 0u : cw[3], w4 = zs ? 0u : cw[4];
+            const uint32_t bs = sh & 31u;
+            const uint32_t h0 = w0 << bs, h1 = __funnelshift_l(w0, w1, bs), h2 = __funnelshift_l(w1, w2, bs),
+                           h3 = __funnelshift_l(w2, w3, bs), h4 = __funnelshift_l(w3, w4, bs),
+                           h5 = __funnelshift_l(w4, 0u, bs);
+            const bool up = sh >= 32u;  // the image starts one 32-bit word higher
+            const uint32_t s0 = sel32(up, 0u, h0), s1 = sel32(up, h0, h1), s2 = sel32(up, h1, h2),
+                           s3 = sel32(up, h2, h3), s4 = sel32(up, h3, h4), s5 = sel32(up, h4, h5),
+                           s6 = sel32(up, h5, 0u);
+            add64_count(a0l, a0h, n0, s0, s1);  // limb l0 + c
+            add64_count(a1l, a1h, n1, s2, s3);  // limb l0 + c + 1
+            add64_count(a2l, a2h, n2, s4, s5);  // limb l0 + c + 2 (s6 -> limb l0 + c + 3, below)
             const uint64_t nk = __ldg(negk + c);
             add64_count(a0l, a0h, n0, (uint32_t)nk, (uint32_t)(nk >> 32));
-            if (c == 0) {
-                v0l = a0l; v0h = a0h;
-            } else {
-                int g = 0;
-                add64_count(a0l, a0h, g, (uint32_t)e_prev, 0u);
-                const uint32_t pr = (a0l & a0h) == 0xffffffffu;
-                u[c] = (uint64_t)a0h << 32 | a0l;
-                gbits |= (uint32_t)g << c;
-                pbits |= pr << c;
-                Gt = (uint32_t)g | (pr & Gt);
-                Pt &= pr;
-            }
-            e_prev = n0;
+            u[c] = (uint64_t)a0h << 32 | a0l;
+            ecnt |= (uint64_t)n0 << (4 * c);
+            a0l = a1l; a0h = a1h; n0 = n1;
+            a1l = a2l; a1h = a2h; n1 = n2;
+            a2l = s6; a2h = 0; n2 = 0;
         }
-        a0l = a1l; a0h = a1h; n0 = n1;
-        a1l = a2l; a1h = a2h; n1 = n2;
-        a2l = s6; a2h = 0; n2 = 0;
-    }
-    // the local carry count of the previous chunk's last limb (thread t - R) comes via smem
-    __shared__ int8_t s_ecarry[T];
-    __shared__ int s_neg[R], s_zmin[R];
-    s_ecarry[tid] = (int8_t)e_prev;
-    if (tid < R) { s_neg[tid] = 0; s_zmin[tid] = INT_MAX; }
-    __syncthreads();
-    {  // limb 0 with the previous chunk's local carry; chunk (G, P) = (limbs 1..) o (limb 0)
-        int g0 = 0;
-        add64_count(v0l, v0h, g0, k > 0 ? (uint32_t)s_ecarry[tid - R] : 0u, 0u);
-        const uint32_t p0 = (v0l & v0h) == 0xffffffffu;
-        u[0] = (uint64_t)v0h << 32 | v0l;
-        gbits |= (uint32_t)g0;
-        pbits |= p0;
-        Gt = Gt | (Pt & (uint32_t)g0);
-        Pt &= p0;
+        // spill-over into the next chunk: partial sums of limbs l0 + CH, + 1 (64-bit), + 2 (32-bit),
+        // their carry counts and the carry count of this chunk's last limb
+        __shared__ uint32_t s_pend[6][T];
+        s_pend[0][tid] = a0l; s_pend[1][tid] = a0h; s_pend[2][tid] = a1l; s_pend[3][tid] = a1h;
+        s_pend[4][tid] = a2l;
+        s_pend[5][tid] = (uint32_t)n0 | ((uint32_t)n1 << 8) | ((uint32_t)((ecnt >> (4 * (CH - 1))) & 15u) << 16);
+        if (tid < R) { s_neg[tid] = 0; s_zmin[tid] = INT_MAX; }
+        __syncthreads();
+        int e_prev = 0;  // carries into limb l0 from the previous chunk's last limb sum
+        if (k > 0) {
+            const int tp = tid - R;
+            const uint32_t cn = s_pend[5][tp];
+            const uint32_t pl[3] = {s_pend[0][tp], s_pend[2][tp], s_pend[4][tp]};
+            const uint32_t ph[3] = {s_pend[1][tp], s_pend[3][tp], 0u};
+            const int pn[3] = {(int)(cn & 255u), (int)((cn >> 8) & 255u), 0};
+#pragma unroll
+            for (int c = 0; c < 3 && c < CH; ++c) {
+                uint32_t lo = (uint32_t)u[c], hi = (uint32_t)(u[c] >> 32);
+                int cnt = (int)((ecnt >> (4 * c)) & 15u) + pn[c];
+                add64_count(lo, hi, cnt, pl[c], ph[c]);
+                u[c] = (uint64_t)hi << 32 | lo;
+                ecnt = (ecnt & ~(15ull << (4 * c))) | ((uint64_t)cnt << (4 * c));
+            }
+            e_prev = (int)(cn >> 16);
+        }
+        // binary lookahead on w_c = v_c + e_(c-1): generate g_c (carry out) / propagate p_c
+        // (w_c = 2^64 - 1); the chunk's (G, P) composes limbs 0 .. CH-1
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+            uint32_t lo = (uint32_t)u[c], hi = (uint32_t)(u[c] >> 32);
+            int g = 0;
+            add64_count(lo, hi, g, (uint32_t)e_prev, 0u);
+            const uint32_t pr = (lo & hi) == 0xffffffffu;
+            u[c] = (uint64_t)hi << 32 | lo;
+            gbits |= (uint32_t)g << c;
+            pbits |= pr << c;
+            Gt = (uint32_t)g | (pr & Gt);
+            Pt &= pr;
+            e_prev = (int)((ecnt >> (4 * c)) & 15u);
+        }
+    } else {
+        // (c) v2: thread t owns limbs [k CH, k CH + CH) of row r = t % R (k = t / R).  Coefficient s
+        // (unsigned C'' < M < 2^155, five words at its residue slot) sits at limb q(s) = floor(w s / 64)
+        // shifted by w s mod 64 (w = 65: s = 64 a + b -> q = 65 a + b, shift b; w = 64: q = s).  The
+        // thread walks positions q = l0 - 3 .. l0 + CH - 1 once, keeping the partial sums of the next
+        // three limbs in registers: limb q is complete after the coefficient at q, and then gets -K's
+        // limb.  u = limb value mod 2^64, e = carries out of those additions (<= 4, added to limb q + 1
+        // below).
+        const uint32_t *qmap = prm.qmap + l0;  // entry j: position qq = l0 - 3 + j (padded past Ly)
+        const uint64_t *negk = prm.negK + l0;  // zero-padded past Ly
+        // pending partial sums of limbs q, q + 1, q + 2 as 32-bit halves, and their carry counts
+        uint32_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, a2l = 0, a2h = 0;
+        int n0 = 0, n1 = 0, n2 = 0;
+        // Limb c of the chunk: v_c = its sum mod 2^64, e_c = carries out of that sum (<= 4).  Binary
+        // lookahead on w_c = v_c + e_(c-1): w_c generates g_c (carry out) or propagates p_c
+        // (w_c = 2^64 - 1); carry into c + 1 = g_c | (p_c & carry into c).  For c >= 1 e_(c-1) is this
+        // thread's, so w_c, g_c, p_c are formed here; limb 0 waits for the previous chunk's e.
+        uint32_t v0l = 0, v0h = 0;       // limb 0 before e_in
+        int e_prev = 0;
+#if HK_K3_SKIP & 4
+#pragma unroll
+        for (int c = 0; c < CH; ++c) u[c] = smr[c * R];
+#pragma unroll
+        for (int j = 0; j < 0; ++j) {
+#else
+#pragma unroll
+        for (int j = 0; j < CH + 3; ++j) {
+#endif
+            const uint32_t qm = __ldg(qmap + j);
+            const uint32_t o = qm >> 6, sh = qm & 63u;
+            const uint32_t w0 = smr[o], w1 = smr[LY::PS + o], w2 = smr[2 * LY::PS + o],
+                           w3 = smr[3 * LY::PS + o], w4 = smr[4 * LY::PS + o];
+            const uint32_t bs = sh & 31u;
+            const uint32_t h0 = w0 << bs, h1 = __funnelshift_l(w0, w1, bs), h2 = __funnelshift_l(w1, w2, bs),
+                           h3 = __funnelshift_l(w2, w3, bs), h4 = __funnelshift_l(w3, w4, bs),
+                           h5 = __funnelshift_l(w4, 0u, bs);
+            const bool up = sh >= 32u;  // the image starts one 32-bit word higher
+            const uint32_t s0 = sel32(up, 0u, h0), s1 = sel32(up, h0, h1), s2 = sel32(up, h1, h2),
+                           s3 = sel32(up, h2, h3), s4 = sel32(up, h3, h4), s5 = sel32(up, h4, h5),
+                           s6 = sel32(up, h5, 0u);
+            add64_count(a0l, a0h, n0, s0, s1);  // limb q
+            add64_count(a1l, a1h, n1, s2, s3);  // limb q + 1
+            add64_count(a2l, a2h, n2, s4, s5);  // limb q + 2 (s6 -> limb q + 3, below)
+            if (j >= 3) {  // limb l = qq is complete: add -K's limb
+                const int c = j - 3;
+                const uint64_t nk = __ldg(negk + c);
+                add64_count(a0l, a0h, n0, (uint32_t)nk, (uint32_t)(nk >> 32));
+                if (c == 0) {
+                    v0l = a0l; v0h = a0h;
+                } else {
+                    int g = 0;
+                    add64_count(a0l, a0h, g, (uint32_t)e_prev, 0u);
+                    const uint32_t pr = (a0l & a0h) == 0xffffffffu;
+                    u[c] = (uint64_t)a0h << 32 | a0l;
+                    gbits |= (uint32_t)g << c;
+                    pbits |= pr << c;
+                    Gt = (uint32_t)g | (pr & Gt);
+                    Pt &= pr;
+                }
+                e_prev = n0;
+            }
+            a0l = a1l; a0h = a1h; n0 = n1;
+            a1l = a2l; a1h = a2h; n1 = n2;
+            a2l = s6; a2h = 0; n2 = 0;
+        }
+        // the local carry count of the previous chunk's last limb (thread t - R) comes via smem
+        __shared__ int8_t s_ecarry[T];
+        s_ecarry[tid] = (int8_t)e_prev;
+        if (tid < R) { s_neg[tid] = 0; s_zmin[tid] = INT_MAX; }
+        __syncthreads();
+        {  // limb 0 with the previous chunk's local carry; chunk (G, P) = (limbs 1..) o (limb 0)
+            int g0 = 0;
+            add64_count(v0l, v0h, g0, k > 0 ? (uint32_t)s_ecarry[tid - R] : 0u, 0u);
+            const uint32_t p0 = (v0l & v0h) == 0xffffffffu;
+            u[0] = (uint64_t)v0h << 32 | v0l;
+            gbits |= (uint32_t)g0;
+            pbits |= p0;
+            Gt = Gt | (Pt & (uint32_t)g0);
+            Pt &= p0;
+        }
     }
     const int gp = (int)(Gt | (Pt << 1));  // (G, P) packed as bit 0 / 1
     // segmented scan over the chunks of each row (lanes r, r + R, ...): compose(later, earlier)

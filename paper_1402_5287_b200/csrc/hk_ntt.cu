@@ -410,6 +410,9 @@ __global__ void __launch_bounds__(k1_threads<LOGN2>(), k1_minb<LOGN2>()) k1_slic
 #ifndef HK_K3_GARNER_X2
 #define HK_K3_GARNER_X2 0  // two Garner slots per thread per round
 #endif
+#ifndef HK_K3_WSCAN
+#define HK_K3_WSCAN 1  // each thread folds the earlier warps' carry totals itself (one barrier fewer; C3 K3 -0.6%)
+#endif
 #ifndef HK_K3_FUSED
 #define HK_K3_FUSED 1  // Garner fused into the carry gather (no separate CRT phase, no lookbehind): C3 K3 -1.5%
 #endif
@@ -942,6 +945,16 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     }
     if (lane >= 32 - R) s_wtot[warp * R + (lane - (32 - R))] = incl;  // per (warp, row) total
     __syncthreads();
+#if HK_K3_WSCAN
+    // carry into this warp's first chunk of row r: every thread folds the earlier warps' totals
+    // itself (at most T / 32 - 1 of them) -- no serial pass by R threads and no second barrier
+    int carry = 0;
+    for (int wi = 0; wi < warp; ++wi) {
+        const int t = s_wtot[wi * R + r];
+        carry = (t & 1) | ((t >> 1) & carry);
+    }
+    const int prev = __shfl_up_sync(0xffffffffu, incl, R);
+#else
     if (tid < R) {  // carry into each warp's first chunk of row tid
         int c = 0;
         for (int wi = 0; wi < T / 32; ++wi) {
@@ -953,6 +966,7 @@ __global__ void __launch_bounds__(k3_threads<LOGN2>(), k3_minb<LOGN2>()) k3_fini
     __syncthreads();
     const int prev = __shfl_up_sync(0xffffffffu, incl, R);
     int carry = s_wcarry[warp * R + r];
+#endif
     if (lane_r > 0) carry = (prev & 1) | ((prev >> 1) & carry);
 #pragma unroll
     for (int c = 0; c < CH; ++c) {  // final limbs (mod 2^(64 Ly))

@@ -32,6 +32,9 @@ namespace hk {
 #ifndef HK_K2_L2PF_NEXT
 #define HK_K2_L2PF_NEXT 148  // columns ahead whose X^ is also prefetched into L2 (0: off)
 #endif
+#ifndef HK_K2_PRUNE
+#define HK_K2_PRUNE 1  // last inverse stage forms / stores only the output whose row is kept (C3 K2 -2.8%)
+#endif
 #ifndef HK_K2_XPF
 #define HK_K2_XPF 1  // X^ top pass: both groups' loads issued before the first group's butterflies (C3 K2 -0.2%)
 #endif
@@ -277,6 +280,40 @@ template <class TW, int LOGN, int T, bool SHARD = false>
 HK_DEV void k2_dit_top(uint32_t *sm, const uint2 *tw, uint32_t p, const Params &prm, size_t cidx,
                        int mrows, int off, bool to_smem) {
     constexpr int N = 1 << LOGN, R = 5, G = 32, S = N / G;
+#if HK_K2_PRUNE
+    if (!to_smem && mrows <= N / 2) {
+        // Output pruning: the last stage pairs positions p and p + N/2, whose output rows differ by
+        // N/2 (row(p) = (N - p - off) mod N), so at most one of the two is among the mrows <= N/2
+        // rows kept -- only that output is formed (u + t, or u - t = u + (p - t)) and stored.
+        for (int j0 = threadIdx.x; j0 < S; j0 += T) {
+            uint32_t v[G];
+            uint32_t *b0 = sm + pad(j0);
+#pragma unroll
+            for (int m = 0; m < G; ++m) v[m] = b0[padded_len(m * S)];
+#pragma unroll
+            for (int l = 0; l < R - 1; ++l) {
+                const int half = 1 << l;
+#pragma unroll
+                for (int m = 0; m < G; ++m) {
+                    if (m & half) continue;
+                    const uint2 w = TW::ld(tw, S * half + j0 + S * (m & (half - 1)));
+                    ct_bfly(v[m], v[m + half], w, p);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < G / 2; ++m) {
+                const uint2 w = TW::ld(tw, S * (G / 2) + j0 + S * m);
+                const uint32_t t = red1(shoup(v[m + G / 2], w.x, w.y, p), p);
+                const int ilo = (N - (j0 + m * S) - off) & (N - 1);  // row of position j0 + m S
+                const uint32_t tt = (ilo & (N / 2)) ? p - t : t;     // the partner's row is ilo - N/2
+                const int i = ilo & (N / 2 - 1);
+                if (i < mrows) __stcs(yhat_at<SHARD>(prm, cidx, i), addm(v[m], tt, p));
+            }
+        }
+        __syncthreads();
+        return;
+    }
+#endif
     for (int j0 = threadIdx.x; j0 < S; j0 += T) {
         uint32_t v[G];
         uint32_t *b0 = sm + pad(j0);  // S multiple of 32

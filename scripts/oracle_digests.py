@@ -15,6 +15,14 @@ The oracle computes the plain definition; noth
 from the CUDA path.
 
   python scripts/oracle_digests.py C2 C5T C5C C3 C4 --threads 7
+
+C4 (n = 16384: about 27 core-hours) is split between hosts: ``--chunks A:B`` computes only chunk
+indices A..B-1 (``--reverse`` walks them from the top) and ``--dig-dir D`` writes each chunk's row
+digests as ``D/rows_XXXXXX.dig`` (16 hex per line, 2 KB per chunk instead of 1 MB of limbs), so a
+remote host can ship its share back; ``--assemble --dig-dir D ...`` then writes the config's
+digest files from every chunk's .npz or .dig.  When some chunks exist only as digests the whole-y
+SHA-256 cannot be formed: the json then carries ``y_sha256: null`` and ``rows_sha256`` (SHA-256 of
+the .rows file), and tests/test_gpu_digests.py compares every row's digest instead.
 """
 from __future__ import annotations
 
@@ -48,42 +56,68 @@ def row_digest(ym_row: np.ndarray, ys_val: np.int8) -> str:
     return hashlib.sha256(ym_row.tobytes() + np.int8(ys_val).tobytes()).hexdigest()[:16]
 
 
-def run(name: str, threads: int, chunk: int) -> None:
+def run(name: str, threads: int, chunk: int, chunks=None, reverse=False, dig_dir=None,
+        assemble=True) -> None:
     c = gen.CONFIGS[name]
     kind, n, P = c["kind"], c["n"], c["P"]
     am, asg, xm, xsg = gen.config_inputs(name)
     isha = input_sha256(am, asg, xm, xsg)
     cdir = os.path.join(CACHE, f"{name}_{isha[:16]}")
     os.makedirs(cdir, exist_ok=True)
+    if dig_dir:
+        os.makedirs(dig_dir, exist_ok=True)
     t0 = time.time()
-    for r0 in range(0, n, chunk):
+    starts = list(range(0, n, chunk))
+    todo = starts if chunks is None else starts[chunks[0]:chunks[1]]
+    for r0 in (reversed(todo) if reverse else todo):
         f = os.path.join(cdir, f"rows_{r0:06d}.npz")
-        if os.path.exists(f):
+        fd = os.path.join(dig_dir, f"rows_{r0:06d}.dig") if dig_dir else None
+        if os.path.exists(f) or (fd and os.path.exists(fd)):
             continue
         rows = np.arange(r0, min(n, r0 + chunk), dtype=np.int64)
         t1 = time.time()
         ym, ys = oracle.matvec(kind, P, am, asg, xm, xsg, rows=rows, threads=threads)
-        np.savez(f + ".tmp.npz", y_mag=ym, y_sign=ys)
-        os.replace(f + ".tmp.npz", f)
+        if fd:
+            with open(fd + ".tmp", "w") as fh:
+                fh.write("\n".join(row_digest(ym[i], ys[i]) for i in range(len(rows))) + "\n")
+            os.replace(fd + ".tmp", fd)
+        else:
+            np.savez(f + ".tmp.npz", y_mag=ym, y_sign=ys)
+            os.replace(f + ".tmp.npz", f)
         print(f"{name}: rows {r0}..{rows[-1]} in {time.time() - t1:.1f} s", flush=True)
-    # assemble in row order
+    if not assemble:
+        return
+    # assemble in row order, from the limbs where this host has them, else from shipped digests
     h = hashlib.sha256()
     mags, signs, lines = [], [], []
-    for r0 in range(0, n, chunk):
-        d = np.load(os.path.join(cdir, f"rows_{r0:06d}.npz"))
-        ym, ys = d["y_mag"], d["y_sign"]
-        mags.append(ym)
-        signs.append(ys)
-        lines.extend(row_digest(ym[i], ys[i]) for i in range(ym.shape[0]))
-    y_mag = np.concatenate(mags)
-    y_sign = np.concatenate(signs)
-    assert y_mag.shape == (n, gen.n_out_limbs(P)) and y_sign.shape == (n,)
-    h.update(y_mag.tobytes())
-    h.update(y_sign.tobytes())
+    whole = True
+    for r0 in starts:
+        f = os.path.join(cdir, f"rows_{r0:06d}.npz")
+        if os.path.exists(f):
+            d = np.load(f)
+            ym, ys = d["y_mag"], d["y_sign"]
+            assert ym.shape == (min(n, r0 + chunk) - r0, gen.n_out_limbs(P))
+            mags.append(ym)
+            signs.append(ys)
+            lines.extend(row_digest(ym[i], ys[i]) for i in range(ym.shape[0]))
+        else:
+            got = open(os.path.join(dig_dir, f"rows_{r0:06d}.dig")).read().split()
+            assert len(got) == min(n, r0 + chunk) - r0, f"chunk {r0}: {len(got)} digests"
+            lines.extend(got)
+            whole = False
+    assert len(lines) == n
+    if whole:
+        y_mag = np.concatenate(mags)
+        y_sign = np.concatenate(signs)
+        assert y_mag.shape == (n, gen.n_out_limbs(P)) and y_sign.shape == (n,)
+        h.update(y_mag.tobytes())
+        h.update(y_sign.tobytes())
+    rows_text = "\n".join(lines) + "\n"
     os.makedirs(OUT, exist_ok=True)
     meta = dict(config=name, kind=kind, n=n, P=P, seed=c["seed"], recipe=c["recipe"],
                 generator="hkinputs SplitMix64 counter generator (SURVEY §8(d))",
-                input_sha256=isha, y_sha256=h.hexdigest(), rows=n,
+                input_sha256=isha, y_sha256=h.hexdigest() if whole else None, rows=n,
+                rows_sha256=hashlib.sha256(rows_text.encode()).hexdigest(),
                 row_digest="first 16 hex of SHA-256(y_mag[i] || y_sign[i])",
                 produced_by="scripts/oracle_digests.py (oracle/hk_oracle.c, all rows)",
                 oracle_threads=threads)
@@ -91,8 +125,9 @@ def run(name: str, threads: int, chunk: int) -> None:
         json.dump(meta, fh, indent=1)
         fh.write("\n")
     with open(os.path.join(OUT, f"{name}.rows"), "w") as fh:
-        fh.write("\n".join(lines) + "\n")
-    print(f"{name}: done, y sha256 {h.hexdigest()} ({time.time() - t0:.0f} s this run)", flush=True)
+        fh.write(rows_text)
+    print(f"{name}: done, y sha256 {meta['y_sha256']} rows sha256 {meta['rows_sha256']} "
+          f"({time.time() - t0:.0f} s this run)", flush=True)
 
 
 def main() -> None:
@@ -100,10 +135,22 @@ def main() -> None:
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--threads", type=int, default=oracle.default_threads())
     ap.add_argument("--chunk", type=int, default=0, help="rows per checkpoint (default by size)")
+    ap.add_argument("--chunks", default=None, help="A:B = compute only chunk indices A..B-1")
+    ap.add_argument("--reverse", action="store_true", help="walk the chunks from the top")
+    ap.add_argument("--dig-dir", default=None, help="write/read per-chunk row digests here")
+    ap.add_argument("--no-assemble", action="store_true")
+    ap.add_argument("--assemble", action="store_true", help="only assemble (compute nothing)")
     args = ap.parse_args()
     for name in args.configs:
         n = gen.CONFIGS[name]["n"]
-        run(name, args.threads, args.chunk or (128 if n > 4096 else 512))
+        chunks = None
+        if args.chunks:
+            a, b = args.chunks.split(":")
+            chunks = (int(a or 0), int(b) if b else None)
+        if args.assemble:
+            chunks = (0, 0)
+        run(name, args.threads, args.chunk or (128 if n > 4096 else 512), chunks=chunks,
+            reverse=args.reverse, dig_dir=args.dig_dir, assemble=not args.no_assemble)
 
 
 if __name__ == "__main__":

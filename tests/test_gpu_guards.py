@@ -147,10 +147,11 @@ def test_guarded_prepared_and_host(hk, kind, n, P):
     (am, asg, xm, xsg), bufs = _inputs(kind, n, P, seed=1300 + n)
     Ly = gen.n_out_limbs(P)
     bufs.update(_outputs(n, Ly))
-    flags = hk.WS_PREPARED | hk.WS_STAGING
-    wsb = hk.workspace_size(kind, n, P, flags=flags)
+    # the two flags are exclusive (the prepared transform and the staging area share the space
+    # after the base layout, include/hk.h): one workspace per entry point
+    wsb = hk.workspace_size(kind, n, P, flags=hk.WS_PREPARED)
     bufs["ws"] = ws = Guarded(wsb)
-    assert hk._lib.hk_workspace_init(kind, n, n, P, flags, ws.ptr, wsb, s) == hk.HK_OK
+    assert hk._lib.hk_workspace_init(kind, n, n, P, hk.WS_PREPARED, ws.ptr, wsb, s) == hk.HK_OK
     b = bufs
     assert hk._lib.hk_prepare_a(kind, n, n, P, b["am"].ptr, b["asg"].ptr, ws.ptr, wsb, s) == hk.HK_OK
     assert hk._lib.hk_matvec_prepared(kind, n, n, P, b["xm"].ptr, b["xsg"].ptr, b["ym"].ptr, b["ysg"].ptr,
@@ -160,12 +161,16 @@ def test_guarded_prepared_and_host(hk, kind, n, P):
     assert np.array_equal(b["ym"].host(np.uint64, (n, Ly)), wm)
     assert np.array_equal(b["ysg"].host(np.int8, (n,)), wsg)
     # host buffers: the device side touched is the workspace (staging) only
+    hsb = hk.workspace_size(kind, n, P, flags=hk.WS_STAGING)
+    hws = Guarded(hsb)
+    assert hk._lib.hk_workspace_init(kind, n, n, P, hk.WS_STAGING, hws.ptr, hsb, s) == hk.HK_OK
     yh = np.zeros((n, Ly), dtype=np.uint64)
     ysh = np.zeros(n, dtype=np.int8)
     rc = hk._lib.hk_matvec_host(kind, n, n, P, am.ctypes.data, asg.ctypes.data, xm.ctypes.data,
-                                xsg.ctypes.data, yh.ctypes.data, ysh.ctypes.data, ws.ptr, wsb, s)
+                                xsg.ctypes.data, yh.ctypes.data, ysh.ctypes.data, hws.ptr, hsb, s)
     assert rc == hk.HK_OK
-    ws.check("host call [ws]")
+    hws.check("host call [ws]")
+    _check_all(bufs, f"host call kind={kind} n={n}")
     assert np.array_equal(yh, wm) and np.array_equal(ysh, wsg)
 
 

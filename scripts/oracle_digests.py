@@ -22,7 +22,8 @@ digests as ``D/rows_XXXXXX.dig`` (16 hex per line, 2 KB per chunk instead of 1 M
 remote host can ship its share back; ``--assemble --dig-dir D ...`` then writes the config's
 digest files from every chunk's .npz or .dig.  When some chunks exist only as digests the whole-y
 SHA-256 cannot be formed: the json then carries ``y_sha256: null`` and ``rows_sha256`` (SHA-256 of
-the .rows file), and tests/test_gpu_digests.py compares every row's digest instead.
+the .rows file), and tests/test_gpu_digests.py compares every row's digest instead.  ``--partial``
+assembles an unfinished run: rows nobody computed carry a placeholder, ``rows_missing`` counts them.
 """
 from __future__ import annotations
 
@@ -56,8 +57,11 @@ def row_digest(ym_row: np.ndarray, ys_val: np.int8) -> str:
     return hashlib.sha256(ym_row.tobytes() + np.int8(ys_val).tobytes()).hexdigest()[:16]
 
 
+MISSING = "-" * 16  # placeholder digest of a row no host has computed yet (--partial)
+
+
 def run(name: str, threads: int, chunk: int, chunks=None, reverse=False, dig_dir=None,
-        assemble=True) -> None:
+        assemble=True, partial=False) -> None:
     c = gen.CONFIGS[name]
     kind, n, P = c["kind"], c["n"], c["P"]
     am, asg, xm, xsg = gen.config_inputs(name)
@@ -101,11 +105,18 @@ def run(name: str, threads: int, chunk: int, chunks=None, reverse=False, dig_dir
             signs.append(ys)
             lines.extend(row_digest(ym[i], ys[i]) for i in range(ym.shape[0]))
         else:
-            got = open(os.path.join(dig_dir, f"rows_{r0:06d}.dig")).read().split()
+            fd = os.path.join(dig_dir, f"rows_{r0:06d}.dig") if dig_dir else None
+            if fd and os.path.exists(fd):
+                got = open(fd).read().split()
+            elif partial:  # an unfinished run: the test checks the rows that exist
+                got = [MISSING] * (min(n, r0 + chunk) - r0)
+            else:
+                raise FileNotFoundError(f"chunk {r0}: neither limbs nor digests (use --partial)")
             assert len(got) == min(n, r0 + chunk) - r0, f"chunk {r0}: {len(got)} digests"
             lines.extend(got)
             whole = False
     assert len(lines) == n
+    missing = sum(1 for d in lines if d == MISSING)
     if whole:
         y_mag = np.concatenate(mags)
         y_sign = np.concatenate(signs)
@@ -117,6 +128,7 @@ def run(name: str, threads: int, chunk: int, chunks=None, reverse=False, dig_dir
     meta = dict(config=name, kind=kind, n=n, P=P, seed=c["seed"], recipe=c["recipe"],
                 generator="hkinputs SplitMix64 counter generator (SURVEY §8(d))",
                 input_sha256=isha, y_sha256=h.hexdigest() if whole else None, rows=n,
+                rows_missing=missing,
                 rows_sha256=hashlib.sha256(rows_text.encode()).hexdigest(),
                 row_digest="first 16 hex of SHA-256(y_mag[i] || y_sign[i])",
                 produced_by="scripts/oracle_digests.py (oracle/hk_oracle.c, all rows)",
@@ -140,6 +152,8 @@ def main() -> None:
     ap.add_argument("--dig-dir", default=None, help="write/read per-chunk row digests here")
     ap.add_argument("--no-assemble", action="store_true")
     ap.add_argument("--assemble", action="store_true", help="only assemble (compute nothing)")
+    ap.add_argument("--partial", action="store_true",
+                    help="assemble even if chunks are missing (their rows get a placeholder digest)")
     args = ap.parse_args()
     for name in args.configs:
         n = gen.CONFIGS[name]["n"]
@@ -150,7 +164,8 @@ def main() -> None:
         if args.assemble:
             chunks = (0, 0)
         run(name, args.threads, args.chunk or (128 if n > 4096 else 512), chunks=chunks,
-            reverse=args.reverse, dig_dir=args.dig_dir, assemble=not args.no_assemble)
+            reverse=args.reverse, dig_dir=args.dig_dir, assemble=not args.no_assemble,
+            partial=args.partial)
 
 
 if __name__ == "__main__":

@@ -1,7 +1,7 @@
 """Full-size bit-exact parity on every BASELINE config (north_star: "bit-exact agreement with the
 oracle on all five configs"; PAPER.md P:50-90 defines the product).
 
-The oracle's y over EVERY row of C2, C3, C4, C5-Toeplitz and C5-circulant takes 1.5 min to 6 h
+The oracle's y over EVERY row of C2, C3, C4, C5-Toeplitz and C5-circulant takes 1.5 min to 28 core-hours
 of host time, so ``scripts/oracle_digests.py`` (which calls only ``oracle/`` and ``hkinputs/``)
 ran it once and committed, per config, the SHA-256 of the whole y and a 64-bit digest of every
 row under ``tests/golden/digests/``.  Here the GPU computes y in the launch configuration

@@ -101,7 +101,15 @@ def test_config_digest(hk, name):
     h = hashlib.sha256()
     h.update(np.ascontiguousarray(gm).tobytes())
     h.update(np.ascontiguousarray(gs).tobytes())
-    assert h.hexdigest() == meta["y_sha256"], f"{name}: FFT-path y differs from the oracle digest"
+    if meta.get("y_sha256"):
+        assert h.hexdigest() == meta["y_sha256"], f"{name}: FFT-path y differs from the oracle digest"
+        return
+    # C4: the oracle run was split between hosts and kept row digests only (scripts/oracle_digests.py)
+    want = open(os.path.join(DIG, f"{name}.rows")).read().split()
+    assert len(want) == gm.shape[0] and meta.get("rows_missing", 0) == 0
+    bad = [i for i, w in enumerate(want)
+           if hashlib.sha256(gm[i].tobytes() + gs[i:i + 1].tobytes()).hexdigest()[:16] != w]
+    assert not bad, f"{name}: FFT-path y differs from the oracle's in {len(bad)} rows, first {bad[:8]}"
 
 
 def test_rejects_bits_above_P(hk):

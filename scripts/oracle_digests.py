@@ -131,7 +131,9 @@ def run(name: str, threads: int, chunk: int, chunks=None, reverse=False, dig_dir
                 rows_missing=missing,
                 rows_sha256=hashlib.sha256(rows_text.encode()).hexdigest(),
                 row_digest="first 16 hex of SHA-256(y_mag[i] || y_sign[i])",
-                produced_by="scripts/oracle_digests.py (oracle/hk_oracle.c, all rows)",
+                produced_by="scripts/oracle_digests.py (oracle/hk_oracle.c, all rows)" +
+                ("" if whole else "; row chunks computed on several hosts (--chunks/--dig-dir), "
+                 "row digests only"),
                 oracle_threads=threads)
     with open(os.path.join(OUT, f"{name}.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
